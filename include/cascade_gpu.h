@@ -1,0 +1,266 @@
+/*
+ * cascade_gpu.h -- C ABI of the B200-native plan-search engine.
+ *
+ * This is the drop-in boundary for the hot path of the Cascade Planner's
+ * bi-level scheduler: batched evaluation of candidate plans, i.e. the body
+ * of cascade::outerplan::sweep and the three entry points it calls.  Every
+ * entry point below replaces exactly one reference C++ interface
+ * (paths relative to the reference tree proj/):
+ *
+ *   cg_sweep              <- cascade::outerplan::sweep
+ *                            include/cascade/outerplan.hpp:89-92, src/outerplan.cpp:166-319
+ *   cg_route              <- cascade::routing::route_trace
+ *                            include/cascade/routing.hpp:26-28, src/routing.cpp:42-93
+ *   cg_stage_row          <- cascade::costmodel::StageEvaluator::row
+ *                            include/cascade/costmodel.hpp:110-111, src/costmodel.cpp:296-414
+ *   cg_solve_min_max      <- cascade::innerplan::solve_min_max
+ *                            include/cascade/innerplan.hpp:63, src/innerplan.cpp:131-194
+ *   cg_generate_trace     <- cascade::cli::generate_trace (synthetic input only)
+ *                            include/cascade/cli.hpp:171-172, src/cli.cpp:428-460
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
+ *     returns a cg_status whose code is CG_OK (-1) on success or the
+ *     reference's cascade::Errc value (include/cascade/errors.hpp:10-18) with
+ *     the reference's own message text.  CG_ERR_CUDA / CG_ERR_UNSUPPORTED are
+ *     engine-only codes.
+ *   - Traces are SoA, stage-major: output_tokens[i*n + r], scores[i*n + r].
+ *     With cg_trace.on_device != 0 all four pointers are device pointers
+ *     (HBM-resident input); otherwise they are host pointers and the engine
+ *     copies them to the GPU inside the call.
+ *   - Output buffers are owned by the library until the matching *_free.
+ *   - One engine per GPU; calls on one engine must not overlap.
+ *   - There is no CPU fallback: if no sm_100 device is present every compute
+ *     entry point fails with CG_ERR_CUDA.
+ */
+#ifndef CASCADE_GPU_H
+#define CASCADE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_OK (-1)
+/* cascade::Errc values (errors.hpp:10-18) */
+#define CG_ERR_INVALID_INPUT 0
+#define CG_ERR_IO 1
+#define CG_ERR_EMPTY_TRACE 2
+#define CG_ERR_NO_DEPLOYED_STAGE 3
+#define CG_ERR_INFEASIBLE 4
+#define CG_ERR_INFEASIBLE_PROBLEM 5
+#define CG_ERR_NO_FEASIBLE_POINT 6
+/* engine-only */
+#define CG_ERR_CUDA 100
+#define CG_ERR_UNSUPPORTED 101
+
+typedef struct cg_status {
+    int32_t code;
+    char message[512];
+} cg_status;
+
+/* cascade::HardwareSpec (domain.hpp:23-33) */
+typedef struct cg_hardware {
+    int32_t gpu_count;
+    double flops_per_gpu;
+    double mem_bandwidth_per_gpu;
+    double mem_capacity_per_gpu;
+    double intra_node_bw;
+    double inter_node_bw;
+    int32_t gpus_per_node;
+} cg_hardware;
+
+/* cascade::ModelSpec (domain.hpp:35-46) */
+typedef struct cg_model {
+    const char* id;
+    double param_count;
+    double bytes_per_param;
+    double kv_bytes_per_token;
+    int32_t min_gpus;
+    int32_t stage_index;
+} cg_model;
+
+/* cascade::costmodel::CostModelParams (costmodel.hpp:27-35) */
+typedef struct cg_cost_params {
+    double prefill_efficiency;
+    double decode_bw_efficiency;
+    double pipeline_bubble_factor;
+    double comm_overhead_per_stage;
+    double kv_memory_fraction;
+    int32_t queueing_sim_requests;
+    uint64_t queueing_sim_seed;
+} cg_cost_params;
+
+/* cascade::WorkloadStats (domain.hpp:48-56) */
+typedef struct cg_workload {
+    double arrival_rate;
+    double mean_input_tokens;
+    double mean_output_tokens;
+    double p95_input_tokens;
+    double p95_output_tokens;
+} cg_workload;
+
+/* std::vector<TraceRecord> (domain.hpp:90-103) as SoA columns. */
+typedef struct cg_trace {
+    int64_t n;
+    int32_t stages;
+    int32_t on_device;            /* 0: host pointers, 1: device pointers */
+    const double* arrival_s;      /* [n] */
+    const double* input_tokens;   /* [n] */
+    const double* output_tokens;  /* [stages][n] */
+    const double* scores;         /* [stages][n] */
+} cg_trace;
+
+/* cascade::outerplan::SweepConfig (outerplan.hpp:56-63).  grid_dims == 0
+ * means "empty threshold_grid" (the reference's default decile grid). */
+typedef struct cg_sweep_config {
+    int32_t grid_dims;
+    const int64_t* grid_sizes;    /* [grid_dims] */
+    const double* grid_values;    /* concatenated, given order kept */
+    double weight_ratio_min;
+    double weight_ratio_max;
+    int32_t weight_count;
+} cg_sweep_config;
+
+typedef struct cg_replica {
+    int32_t tp;
+    int32_t pp;
+} cg_replica;
+
+/* cascade::ParallelismPlan (domain.hpp:67-72): replicas[offset .. offset+dp) */
+typedef struct cg_plan {
+    int32_t gpus_used;
+    int32_t dp;
+    int64_t replica_offset;
+} cg_plan;
+
+/* Engine-side counters and per-phase device times of the last sweep. */
+typedef struct cg_sweep_stats {
+    int64_t candidates;           /* threshold vectors in the grid */
+    int64_t distinct_candidates;  /* after collapsing duplicate grid values */
+    int64_t stage_workloads;      /* (stage, threshold-prefix) workloads routed */
+    int64_t unique_rows;          /* latency rows evaluated (reference row cache) */
+    int64_t plans_enumerated;     /* sum over rows of |plan set| */
+    int64_t plans_stable;         /* plans passing the stability filter */
+    int64_t plans_simulated_full; /* 2000-request simulations run to completion */
+    int64_t plans_pruned;         /* simulations stopped by the exact p95 bound */
+    int64_t plans_overflow;       /* re-run by the deep-queue kernel */
+    int64_t request_steps;        /* JSQ dispatch steps executed */
+    int64_t h2d_bytes;
+    int64_t d2h_bytes;
+    int32_t num_ranks;
+    int32_t gpu_launches;         /* engine kernels launched by this call */
+    double ms_total;              /* host wall time of the call */
+    double ms_route;              /* K1-K3: routing / aggregation / p95 */
+    double ms_quality;            /* K2: trace-order quality sums */
+    double ms_rows;               /* K4-K5: cost-model rows */
+    double ms_solve;              /* K6-K7: min-max solve, Tchebycheff, Pareto */
+    double ms_k1;                 /* the routing/aggregation pass alone */
+    double k1_bytes;              /* algorithmic bytes moved by that pass */
+    double ms_k4;                 /* the queueing-simulation kernels alone */
+} cg_sweep_stats;
+
+/* cascade::outerplan::SweepResult (outerplan.hpp:73-80), flattened. */
+typedef struct cg_sweep_result {
+    int32_t stages;                 /* C */
+    double z1_star;                 /* UtopiaPoint */
+    double z2_star;
+    int64_t num_evaluations;        /* E, grid order */
+    int64_t* eval_candidate;        /* [E] cartesian index, first dim outermost */
+    double* eval_thresholds;        /* [E][C-1] */
+    double* eval_latency;           /* [E] L */
+    double* eval_quality;           /* [E] Q */
+    double* eval_ratios;            /* [E][C] processing_ratios */
+    int32_t* eval_allocations;      /* [E][C] */
+    int64_t* eval_plan;             /* [E][C] index into plans, -1 = nullopt */
+    int64_t num_plans;
+    cg_plan* plans;
+    int64_t num_replicas;
+    cg_replica* replicas;
+    int32_t num_weights;
+    double* weights;                /* [W][2] lambda1, lambda2 */
+    int32_t* weight_selection;      /* [W] index into evaluations */
+    int64_t front_size;
+    int64_t* front;                 /* [F] index into evaluations, latency asc */
+    int64_t num_skipped;
+    int64_t* skipped_candidate;     /* [S] cartesian index */
+    double* skipped_thresholds;     /* [S][C-1] */
+    cg_sweep_stats stats;
+} cg_sweep_result;
+
+/* Host-side all-gather over device buffers, used by multi-GPU sweeps: must
+ * gather `bytes_per_rank` bytes from every rank into recv (rank-major) and
+ * return 0 on success.  Called on the engine's stream, which is synchronised
+ * before the call. */
+typedef int (*cg_allgather_fn)(const void* send_dev, void* recv_dev, size_t bytes_per_rank,
+                               void* user);
+
+typedef struct cg_engine cg_engine;
+
+cg_status cg_engine_create(int32_t device, cg_engine** out);
+void cg_engine_destroy(cg_engine* engine);
+/* Shard the cost-model work over `world` ranks (this engine is `rank`). */
+cg_status cg_engine_set_collective(cg_engine* engine, int32_t rank, int32_t world,
+                                   cg_allgather_fn allgather, void* user);
+/* Debug/parity knob: 0 disables the exact p95-bound pruning in K4. */
+cg_status cg_engine_set_option(cg_engine* engine, const char* key, int64_t value);
+
+cg_status cg_sweep(cg_engine* engine, const cg_trace* trace, const cg_model* models,
+                   int32_t num_models, const cg_hardware* hw, const cg_cost_params* params,
+                   int32_t total_gpus, const cg_sweep_config* cfg, cg_sweep_result** out);
+void cg_sweep_result_free(cg_sweep_result* result);
+
+/* cascade::routing::RoutingOutcome (routing.hpp:15-20). */
+typedef struct cg_route_result {
+    int32_t stages;
+    double ratios[8];
+    cg_workload stage_workloads[8];
+    double quality;
+} cg_route_result;
+
+/* route_trace with a deployment mask (deployed[i] != 0).  accept_stage, if
+ * non-NULL, receives the 1-based accept stage of every request (host). */
+cg_status cg_route(cg_engine* engine, const cg_trace* trace, const double* thresholds,
+                   const int32_t* deployed, cg_route_result* out, int32_t* accept_stage);
+
+/* StageEvaluator::row: latency[f] for f in 0..max_budget (INFINITY when
+ * infeasible) and plan_index[f] (-1 = nullopt) into *plans / *replicas. */
+typedef struct cg_row_result {
+    int32_t max_budget;
+    double* latency;                /* [max_budget+1] */
+    int64_t* plan_index;            /* [max_budget+1] */
+    int64_t num_plans;
+    cg_plan* plans;
+    int64_t num_replicas;
+    cg_replica* replicas;
+    cg_sweep_stats stats;
+} cg_row_result;
+
+cg_status cg_stage_row(cg_engine* engine, const cg_model* model, const cg_workload* w,
+                       const cg_hardware* hw, const cg_cost_params* params,
+                       int32_t max_budget, cg_row_result** out);
+void cg_row_result_free(cg_row_result* result);
+
+/* solve_min_max on a latency table entries[i*(gpu_budget+1) + f]
+ * (INFINITY = masked cell).  Writes allocations[stages], per_stage[stages]
+ * and *objective_L. */
+cg_status cg_solve_min_max(cg_engine* engine, const double* entries, int32_t stages,
+                           int32_t gpu_budget, int32_t total_gpus, int32_t* allocations,
+                           double* per_stage_latency, double* objective_L);
+
+/* Synthetic trace generation with the reference generator's semantics and
+ * bit-identical output.  spec_json is the TraceGenSpec JSON
+ * (cli.hpp:141-169).  Host buffers of capacity >= count (and
+ * stages*count for the per-stage columns); *n_out = count. */
+cg_status cg_generate_trace(const char* spec_json, uint64_t seed, double* arrival_s,
+                            double* input_tokens, double* output_tokens, double* scores,
+                            int64_t capacity, int64_t* n_out, int32_t* stages_out);
+
+const char* cg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CASCADE_GPU_H */

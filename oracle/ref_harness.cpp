@@ -1,0 +1,297 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product.
+//
+// extern "C" harness over the UNMODIFIED reference planner (compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/).  Tests,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+// call it through ctypes to (a) obtain ground-truth results of the
+// reference's own entry points and (b) time the reference CPU scheduler.
+//
+// Entry points wrapped (reference file:line):
+//   cascade::outerplan::sweep            proj/include/cascade/outerplan.hpp:89-92
+//   cascade::routing::route_trace        proj/include/cascade/routing.hpp:26-28
+//   cascade::costmodel::StageEvaluator::row  proj/include/cascade/costmodel.hpp:110-111
+//   cascade::innerplan::solve_min_max    proj/include/cascade/innerplan.hpp:63
+//   cascade::cli::generate_trace         proj/include/cascade/cli.hpp:171-172
+//
+// Every function returns a malloc'd JSON string (free with ref_free):
+//   {"ok":true,"result":<reference to_json of the result>,"elapsed_s":t}
+//   {"ok":false,"code":<int Errc>,"code_name":"...","message":"..."}
+#include <chrono>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "cascade/cli.hpp"
+#include "cascade/costmodel.hpp"
+#include "cascade/innerplan.hpp"
+#include "cascade/outerplan.hpp"
+#include "cascade/routing.hpp"
+#include "cascade/util.hpp"
+
+using nlohmann::json;
+using namespace cascade;
+
+namespace {
+
+char* dup(const std::string& s) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.data(), s.size() + 1);
+    return p;
+}
+
+char* ok(json result, double elapsed) {
+    json j;
+    j["ok"] = true;
+    j["result"] = std::move(result);
+    j["elapsed_s"] = elapsed;
+    return dup(j.dump());
+}
+
+char* fail(const CascadeError& e) {
+    json j;
+    j["ok"] = false;
+    j["code"] = static_cast<int>(e.code());
+    j["code_name"] = e.code_name();
+    j["message"] = e.what();
+    return dup(j.dump());
+}
+
+char* fail_std(const std::exception& e) {
+    json j;
+    j["ok"] = false;
+    j["code"] = 100;
+    j["code_name"] = "STD_EXCEPTION";
+    j["message"] = e.what();
+    return dup(j.dump());
+}
+
+std::vector<TraceRecord> make_trace(const double* arrival, const double* in_tok,
+                                    const double* out_tok, const double* scores,
+                                    std::int64_t n, int c) {
+    std::vector<TraceRecord> trace(static_cast<std::size_t>(n));
+    for (std::int64_t r = 0; r < n; ++r) {
+        auto& rec = trace[r];
+        rec.arrival_s = arrival[r];
+        rec.input_tokens = in_tok[r];
+        rec.per_stage.resize(c);
+        for (int i = 0; i < c; ++i) {
+            rec.per_stage[i].output_tokens = out_tok[static_cast<std::int64_t>(i) * n + r];
+            rec.per_stage[i].score = scores[static_cast<std::int64_t>(i) * n + r];
+        }
+    }
+    return trace;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_free(char* p) { std::free(p); }
+
+/// config_json: {"hardware":{..},"models":[..],"cost_model":{..},"sweep":{..}}
+/// (the reference PlannerConfig schema, cli.cpp:48-80).  Times sweep() only.
+char* ref_sweep(const double* arrival, const double* in_tok, const double* out_tok,
+                const double* scores, std::int64_t n, int c, const char* config_json,
+                int total_gpus) {
+    try {
+        auto cfg = json::parse(config_json).get<cli::PlannerConfig>();
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        auto t0 = std::chrono::steady_clock::now();
+        auto res = outerplan::sweep(trace, cfg.models, cfg.hardware, cfg.cost_model,
+                                    total_gpus, cfg.sweep);
+        double el = seconds_since(t0);
+        return ok(json(res), el);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// sweep + select_plan + the CLI file payloads (cli.cpp:165-175), dumped
+/// exactly as cmd_plan writes them (dump(2) + "\n", front_to_csv).
+char* ref_plan_outputs(const double* arrival, const double* in_tok,
+                       const double* out_tok, const double* scores, std::int64_t n,
+                       int c, const char* config_json, int total_gpus,
+                       const char* requirement_json) {
+    try {
+        auto cfg = json::parse(config_json).get<cli::PlannerConfig>();
+        auto rq = json::parse(requirement_json);
+        outerplan::PlanRequirement req;
+        if (rq.contains("min_quality")) req.min_quality = rq["min_quality"].get<double>();
+        if (rq.contains("max_latency")) req.max_latency = rq["max_latency"].get<double>();
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        auto res = outerplan::sweep(trace, cfg.models, cfg.hardware, cfg.cost_model,
+                                    total_gpus, cfg.sweep);
+        auto plan = outerplan::select_plan(res.front, req);
+        json files;
+        files["plan.json"] = json(plan).dump(2) + "\n";
+        files["front.json"] = json(res.front).dump(2) + "\n";
+        files["front.csv"] = outerplan::front_to_csv(res.front);
+        files["sweep.json"] = json(res).dump(2) + "\n";
+        return ok(files, 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+char* ref_route(const double* arrival, const double* in_tok, const double* out_tok,
+                const double* scores, std::int64_t n, int c, const double* thresholds,
+                const int* deployed) {
+    try {
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        RoutingThresholds h;
+        h.thresholds.assign(thresholds, thresholds + (c > 0 ? c - 1 : 0));
+        std::vector<bool> dep(c);
+        for (int i = 0; i < c; ++i) dep[i] = deployed[i] != 0;
+        auto t0 = std::chrono::steady_clock::now();
+        auto out = routing::route_trace(trace, h, dep);
+        double el = seconds_since(t0);
+        json j;
+        j["ratios"] = out.ratios;
+        j["stage_workloads"] = out.stage_workloads;
+        j["quality"] = out.quality;
+        j["per_request_accept_stage"] = out.per_request_accept_stage;
+        return ok(j, el);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// One StageEvaluator::row (costmodel.cpp:296-414).
+char* ref_row(const char* hw_json, const char* params_json, const char* model_json,
+              const char* workload_json, int max_budget) {
+    try {
+        auto hw = json::parse(hw_json).get<HardwareSpec>();
+        auto params = json::parse(params_json).get<costmodel::CostModelParams>();
+        auto model = json::parse(model_json).get<ModelSpec>();
+        auto w = json::parse(workload_json).get<WorkloadStats>();
+        costmodel::StageEvaluator ev(hw, params);
+        auto t0 = std::chrono::steady_clock::now();
+        auto row = ev.row(model, w, max_budget);
+        double el = seconds_since(t0);
+        json lat = json::array();
+        for (double v : row.latency) {
+            if (std::isinf(v)) lat.push_back(nullptr);
+            else lat.push_back(v);
+        }
+        json plans = json::array();
+        for (const auto& p : row.plan) {
+            if (p) plans.push_back(*p);
+            else plans.push_back(nullptr);
+        }
+        json j;
+        j["latency"] = lat;
+        j["plan"] = plans;
+        return ok(j, el);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// innerplan::solve_min_max on a LatencyTable in its JSON "profile" format
+/// (innerplan.cpp:14-56; null = infeasible).
+char* ref_solve(const char* table_json, int total_gpus) {
+    try {
+        auto table = json::parse(table_json).get<innerplan::LatencyTable>();
+        auto sol = innerplan::solve_min_max(table, total_gpus);
+        json j;
+        j["allocations"] = sol.allocations;
+        j["objective_L"] = sol.objective_L;
+        j["per_stage_latency"] = sol.per_stage_latency;
+        return ok(j, 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+char* ref_export_milp(const char* table_json, int total_gpus) {
+    try {
+        auto table = json::parse(table_json).get<innerplan::LatencyTable>();
+        return ok(json(innerplan::export_milp(table, total_gpus)), 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// cli::generate_trace (cli.cpp:428-460) into caller-owned SoA buffers
+/// sized count and stages*count (stage-major).  Returns the error JSON or
+/// an ok JSON with the count.
+char* ref_generate_trace(const char* spec_json, std::uint64_t seed, double* arrival,
+                         double* in_tok, double* out_tok, double* scores,
+                         std::int64_t capacity) {
+    try {
+        auto spec = json::parse(spec_json).get<cli::TraceGenSpec>();
+        auto trace = cli::generate_trace(spec, seed);
+        const std::int64_t n = static_cast<std::int64_t>(trace.size());
+        if (n > capacity) throw std::runtime_error("capacity too small");
+        const int c = static_cast<int>(spec.stages.size());
+        for (std::int64_t r = 0; r < n; ++r) {
+            arrival[r] = trace[r].arrival_s;
+            in_tok[r] = trace[r].input_tokens;
+            for (int i = 0; i < c; ++i) {
+                out_tok[static_cast<std::int64_t>(i) * n + r] =
+                    trace[r].per_stage[i].output_tokens;
+                scores[static_cast<std::int64_t>(i) * n + r] = trace[r].per_stage[i].score;
+            }
+        }
+        return ok(json(n), 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// Weight ladder, default grid and utopia helpers, for unit-level parity.
+char* ref_weight_ladder(double rmin, double rmax, int count) {
+    try {
+        outerplan::SweepConfig cfg;
+        cfg.weight_ratio_min = rmin;
+        cfg.weight_ratio_max = rmax;
+        cfg.weight_count = count;
+        return ok(json(outerplan::weight_ladder(cfg)), 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+char* ref_pareto(const double* latency, const double* quality, std::int64_t n) {
+    try {
+        std::vector<ObjectivePoint> pts(static_cast<std::size_t>(n));
+        for (std::int64_t i = 0; i < n; ++i) {
+            pts[i].latency_s = latency[i];
+            pts[i].quality = quality[i];
+            pts[i].plan_ref.predicted_max_p95_s = static_cast<double>(i);  // index tag
+        }
+        auto front = outerplan::pareto_filter(pts);
+        json idx = json::array();
+        for (const auto& p : front.points)
+            idx.push_back(static_cast<std::int64_t>(p.plan_ref.predicted_max_p95_s));
+        return ok(idx, 0.0);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+int ref_max_threads() { return util::max_threads(); }
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// Kernel argument blocks and host-side launchers (implemented in k_*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "cg_internal.h"
+
+namespace cg {
+
+// ---------------- routing (k_route.cu)
+struct RouteArgs {
+    long long n;
+    const double* scores;  // [C][n]
+    const double* in;      // [n]
+    const double* out;     // [C][n]
+    const double* gvals;   // distinct sorted grid values, concatenated
+    int goff[4];
+    int G[4];
+    int gtotal;
+    int grid_in_smem;
+    long long stride[4];   // histogram strides (dim 0 fastest, extent G+1)
+    unsigned long long* ranks;  // [n] packed 16-bit ranks
+    unsigned long long* hist;   // [cells][2+C]
+    unsigned int* flags;        // bit0: a token is not an integer in [0, 2^32)
+};
+
+struct WorkloadArgs {
+    int C;
+    long long total;        // sum over stages of P_i
+    long long wl_off[kMaxStages + 1];
+    int G[4];
+    long long stride[4];
+    const unsigned long long* hist;
+    unsigned long long* count;
+    unsigned long long* sum_in;
+    unsigned long long* sum_out;
+};
+
+void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches);
+void launch_hist_scan(unsigned long long* hist, long long cells, int Q, const long long* stride,
+                      const int* G, int D, cudaStream_t s, int* launches);
+void launch_workload_counts(const WorkloadArgs& a, cudaStream_t s, int* launches);
+void launch_workload_seq_sums(const WorkloadArgs& a, const unsigned long long* ranks, const double* in,
+                              const double* out, long long n, double* sum_in_f, double* sum_out_f,
+                              cudaStream_t s, int* launches);
+void launch_make_lists(const double* in, const double* out, const unsigned long long* ranks, long long n,
+                       int C, unsigned long long* keys, unsigned long long* vals, int sm_count,
+                       cudaStream_t s, int* launches);
+void launch_p95_scan(const WorkloadArgs& a, const unsigned long long* keys, const unsigned long long* vals,
+                     long long n, double* p95_in, double* p95_out, cudaStream_t s, int* launches);
+void launch_workload_stats(const WorkloadArgs& a, long long n, double rate, int integral,
+                           const double* sum_in_f, const double* sum_out_f, const double* p95_in,
+                           const double* p95_out, double* stats, cudaStream_t s, int* launches);
+void launch_quality(const double* scores, long long n, int D, const double* thr, long long ncand,
+                    double* qsum, cudaStream_t s, int* launches);
+
+// ---------------- sort (k_sort.cu)
+void launch_or_and(const unsigned long long* keys, long long n, unsigned long long* out2, cudaStream_t s,
+                   int* launches);
+// Returns 1 when the sorted data ended in the *_tmp buffers.
+int radix_sort_u64(unsigned long long* keys, unsigned long long* vals, unsigned long long* keys_tmp,
+                   unsigned long long* vals_tmp, long long n, unsigned long long varying_bits,
+                   unsigned int* hist_scratch, cudaStream_t s, int* launches);
+size_t radix_hist_entries(long long n);
+
+// ---------------- cost model (k_cost.cu)
+struct ModelArgs {
+    double param_count, bytes_per_param, kv_bytes_per_token;
+};
+struct HwArgs {
+    double flops, mem_bandwidth, mem_capacity;
+};
+struct ParamArgs {
+    double prefill_efficiency, decode_bw_efficiency, pipeline_bubble_factor, comm_overhead_per_stage,
+        kv_memory_fraction;
+};
+
+struct RowSetupArgs {
+    int nrows;
+    int n_req;
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    const ModelArgs* models;
+    HwArgs hw;
+    ParamArgs p;
+    RowTables tab;
+};
+
+enum : int { CTR_STABLE = 0, CTR_FULL = 1, CTR_PRUNED = 2, CTR_STEPS = 3, CTR_COUNT = 8 };
+
+struct SimArgs {
+    int N, n_req, K, prune, item_plans;
+    int nrows;                                 // rows of this class
+    const int* row_ids;                        // class rows -> global row index
+    const unsigned long long* item_prefix;     // [nrows+1] cumulative item counts
+    unsigned long long nitems;
+    unsigned long long* item_counter;
+    const SimItem* deep_items;                 // DEEP: one plan per item
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    RowTables tab;
+    unsigned long long* lat_min;               // [row][N+1] latency bits, exact per-budget min
+    unsigned long long* ub;                    // [row][N+1] prefix-min bound for pruning
+    TieEntry* ties;
+    unsigned long long* tie_count;
+    unsigned long long tie_cap;
+    SimItem* ovf;
+    unsigned long long* ovf_count;
+    unsigned long long ovf_cap;
+    double* scratch;                           // [slots][n_req]
+    double* ring_global;                       // DEEP: [warps][32*R*ring_cap]
+    int ring_cap;
+    unsigned long long* counters;
+};
+
+struct SimGeometry {
+    int W, R, G, grid;
+    long long slots, warps;
+};
+
+int class_for_dp(int dpmax);
+void class_shape(int cls, int* W, int* R);
+SimGeometry sim_geometry(int cls, bool deep, int sm_count);
+void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches);
+void launch_sim(const SimArgs& a, int cls, bool deep, int sm_count, cudaStream_t s, int* launches,
+                int* grid_out);
+
+struct ResolveArgs {
+    int N, nrows;
+    unsigned long long nties;
+    const TieEntry* ties;
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    const unsigned long long* lat_min;
+    unsigned long long* best_plan;   // [row][N+1], ~0 = empty
+    double* final_lat;               // [row][N+1]
+    long long* final_plan;           // [row][N+1]
+};
+void launch_resolve(const ResolveArgs& a, cudaStream_t s, int* launches);
+
+// ---------------- solve (k_solve.cu)
+struct SolveArgs {
+    int C, N, total_gpus;
+    int raw_f0;              // 1: use cell f=0 as given (standalone solve)
+    long long ntuples;
+    long long wl_off[kMaxStages + 1];
+    long long wl_P[kMaxStages];
+    const unsigned long long* wl_count;
+    const int* wl_row;
+    const double* final_lat;
+    const long long* final_plan;
+    unsigned char* feasible;
+    double* L;
+    int* alloc;        // [t][C]
+    long long* plan;   // [t][C]
+};
+void launch_solve(const SolveArgs& a, cudaStream_t s, int* launches);
+
+struct ExpandArgs {
+    int D;
+    long long ncand;
+    int Gg[4];               // given grid sizes
+    int Gd[4];               // distinct sizes
+    int goff[4];             // offsets into g2d
+    const int* g2d;          // given index -> distinct index
+    const unsigned char* tuple_feasible;
+    long long* cand_tuple;
+    unsigned* flag;
+};
+void launch_expand(const ExpandArgs& a, unsigned* pos, unsigned long long* total, const double* tuple_L,
+                   const double* tuple_qsum, double n, long long* eval_cand, double* eval_L,
+                   double* eval_Q, long long* skip_cand, cudaStream_t s, int* launches);
+void launch_tchebycheff(const double* L, const double* Q, long long E, const double* weights, int nw,
+                        double z1, double z2, int* sel, cudaStream_t s, int* launches);
+void launch_pareto(const double* L, const double* Q, long long E, unsigned long long* k0,
+                   unsigned long long* k1, unsigned long long* v0, unsigned long long* v1,
+                   unsigned long long* kl, unsigned long long* orax, unsigned int* hist, long long* front,
+                   long long* front_size, cudaStream_t s, int* launches);
+
+}  // namespace cg

@@ -1,0 +1,1305 @@
+// Host orchestration of the plan-search engine behind the C ABI
+// (include/cascade_gpu.h).  Mirrors cascade::outerplan::sweep
+// (proj/src/outerplan.cpp:166-319) phase by phase:
+//
+//   validation (same order and messages as the reference)
+//   -> trace to HBM -> threshold grid (explicit, or default deciles on GPU)
+//   -> K1-K3 routing of every (stage, threshold-prefix) workload at once
+//   -> K2 trace-order quality of every distinct threshold tuple
+//   -> workload validation in candidate order + row-cache dedup (host, exact bits)
+//   -> K4-K5 latency rows for every unique workload (sharded over ranks,
+//      merged with one all-gather)
+//   -> utopia check -> K6 min-max solve per tuple -> grid-order expansion
+//   -> K7 Tchebycheff argmin per weight, Pareto front -> SweepResult.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "cascade_gpu.h"
+#include "cg_cuda.h"
+#include "cg_internal.h"
+#include "cg_kernels.h"
+#include "host_model.h"
+#include "plan_dev.cuh"
+
+using namespace cg;
+
+namespace {
+
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+constexpr double kThresholdSentinel = 101.0;  // domain.hpp:21
+
+double dinf() { return std::numeric_limits<double>::infinity(); }
+
+cg_status ok_status() {
+    cg_status s;
+    s.code = CG_OK;
+    s.message[0] = 0;
+    return s;
+}
+
+cg_status err_status(int code, const std::string& msg) {
+    cg_status s;
+    s.code = code;
+    std::snprintf(s.message, sizeof(s.message), "%s", msg.c_str());
+    return s;
+}
+
+template <class F>
+cg_status guarded(F&& f) {
+    try {
+        f();
+        return ok_status();
+    } catch (const EngineError& e) {
+        return err_status(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        return err_status(CG_ERR_CUDA, "host allocation failed");
+    } catch (const std::exception& e) {
+        return err_status(CG_ERR_CUDA, e.what());
+    }
+}
+
+struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double ms() const {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+__global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+__global__ void k_score_keys(const double* __restrict__ s, long long n, unsigned long long* __restrict__ k) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) k[i] = dbl_to_key(s[i]);
+}
+
+// route_trace accept stage (routing.cpp:65-81), 1-based
+__global__ void k_accept_stage(const double* __restrict__ scores, long long n, int C,
+                               const double* __restrict__ h, int last, const int* __restrict__ deployed,
+                               int* __restrict__ out) {
+    const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int acc = last;
+    for (int i = 0; i < C; ++i) {
+        if (!deployed[i]) continue;
+        if (i == last) break;
+        if (scores[(long long)i * n + r] >= h[i]) {
+            acc = i;
+            break;
+        }
+    }
+    out[r] = acc + 1;
+}
+
+// Cross-rank merge of per-budget bests: minimum latency; equal latency ->
+// parts-lexicographic minimum plan (the reference's `better`, costmodel.cpp:347-352).
+// Gathered layout: rank r occupies [r*2*cells, (r+1)*2*cells): lat bits, then plan.
+__global__ void k_merge_ranks(const unsigned long long* __restrict__ gathered, int world, long long cells,
+                              int N, const RowDesc* __restrict__ rows, const PlanSpace* __restrict__ spaces,
+                              unsigned long long* __restrict__ lat_out, unsigned long long* __restrict__ plan_out) {
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const int row = (int)(c / (N + 1));
+    const PlanSpace& sp = spaces[rows[row].space];
+    unsigned long long bl = kInfBits, bp = ~0ull;
+    unsigned char A[kMaxShapes], B[kMaxShapes];
+    for (int r = 0; r < world; ++r) {
+        const unsigned long long l = gathered[(long long)r * 2 * cells + c];
+        const unsigned long long p = gathered[(long long)r * 2 * cells + cells + c];
+        if (p == ~0ull) continue;
+        bool take = false;
+        if (bp == ~0ull || l < bl) {
+            take = true;
+        } else if (l == bl && p != bp) {
+            unrank_plan(sp, p, A);
+            unrank_plan(sp, bp, B);
+            take = parts_less(A, B, sp.S);
+        }
+        if (take) {
+            bl = l;
+            bp = p;
+        }
+    }
+    lat_out[c] = bl;
+    plan_out[c] = bp;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+struct cg_engine {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t s = nullptr;
+    int rank = 0, world = 1;
+    cg_allgather_fn allgather = nullptr;
+    void* ag_user = nullptr;
+    int prune = 1;
+    int item_plans = 128;
+    long long ovf_cap = 1 << 20;
+    long long tie_cap = 1 << 22;
+    cudaEvent_t ev[16];
+
+    DevBuf d_scores, d_in, d_out;
+    DevBuf d_gvals, d_ranks, d_hist, d_flags, d_lk0, d_lv0, d_lk1, d_lv1, d_rshist, d_orax;
+    DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
+    DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_T, d_O, d_crn;
+    DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
+        d_scratch, d_ring, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
+    DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_acc;
+};
+
+namespace {
+
+struct SweepCtx {
+    cg_engine& E;
+    cudaStream_t s;
+    int launches = 0;
+    cg_sweep_stats st{};
+    explicit SweepCtx(cg_engine& e) : E(e), s(e.s) {}
+
+    void d2h(void* dst, const void* src, size_t bytes) {
+        if (!bytes) return;
+        CG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        st.d2h_bytes += (long long)bytes;
+    }
+    void h2d(void* dst, const void* src, size_t bytes) {
+        if (!bytes) return;
+        CG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        st.h2d_bytes += (long long)bytes;
+    }
+    void sync() { CG_CUDA(cudaStreamSynchronize(s)); }
+    void fill(unsigned long long* p, long long n, unsigned long long v) {
+        if (n <= 0) return;
+        k_fill_u64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, v);
+        CG_LAUNCH_CHECK();
+        ++launches;
+    }
+};
+
+// Plan spaces of every model at budget N (host tables, uploaded).
+std::vector<HostPlanSpace> build_spaces(SweepCtx& x, const cg_model* models, int C, const cg_hardware& hw,
+                                        const cg_cost_params& q, int N) {
+    std::vector<HostPlanSpace> hs(C);
+    std::vector<PlanSpace> dsp(C);
+    size_t ways_total = 0;
+    for (int i = 0; i < C; ++i) {
+        auto shapes = legal_shapes(models[i], hw, q);
+        if ((int)shapes.size() > kMaxShapes) fail(CG_ERR_UNSUPPORTED, "too many replica shapes");
+        hs[i].build(std::move(shapes), N);
+        ways_total += hs[i].ways.size();
+    }
+    unsigned long long* dways = x.E.d_ways.as<unsigned long long>(ways_total);
+    size_t off = 0;
+    for (int i = 0; i < C; ++i) {
+        PlanSpace& p = dsp[i];
+        std::memset(&p, 0, sizeof(p));
+        p.S = (int)hs[i].shapes.size();
+        p.N = hs[i].N;
+        for (int k = 0; k < p.S; ++k) p.shapes[k] = hs[i].shapes[k];
+        p.ways = dways + off;
+        p.num_plans = hs[i].num_plans;
+        x.h2d(dways + off, hs[i].ways.data(), hs[i].ways.size() * sizeof(unsigned long long));
+        off += hs[i].ways.size();
+    }
+    x.h2d(x.E.d_spaces.as<PlanSpace>(C), dsp.data(), sizeof(PlanSpace) * C);
+    std::vector<ModelArgs> ma(C);
+    for (int i = 0; i < C; ++i)
+        ma[i] = {models[i].param_count, models[i].bytes_per_param, models[i].kv_bytes_per_token};
+    x.h2d(x.E.d_models.as<ModelArgs>(C), ma.data(), sizeof(ModelArgs) * C);
+    return hs;
+}
+
+int row_class(const HostPlanSpace& sp, int N) {
+    if (sp.min_gpus <= 0 || N < 1) return 3;
+    const int dpmax = N / sp.min_gpus;
+    const int cls = class_for_dp(dpmax);
+    if (cls < 0) fail(CG_ERR_UNSUPPORTED, "plans with more than 256 replicas are not supported");
+    return cls;
+}
+
+// K4-K5 for a set of unique rows.  Afterwards E.d_flat / E.d_fplan hold the
+// final [row][N+1] latency / plan index (merged across ranks).
+void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vector<HostPlanSpace>& hs,
+                   const cg_hardware& hw, const cg_cost_params& q, int N) {
+    cg_engine& E = x.E;
+    const int nrows = (int)rows.size();
+    const long long cells = (long long)nrows * (N + 1);
+    const int n_req = q.queueing_sim_requests;
+    if (nrows == 0) return;
+    x.h2d(E.d_rows.as<RowDesc>(nrows), rows.data(), sizeof(RowDesc) * nrows);
+
+    RowTables tab;
+    tab.shape_ok = E.d_ok.as<unsigned char>((size_t)nrows * kMaxShapes);
+    tab.prefill = E.d_pre.as<double>((size_t)nrows * kMaxShapes);
+    tab.decode = E.d_dec.as<double>((size_t)nrows * kMaxShapes);
+    tab.mean_service = E.d_ms.as<double>((size_t)nrows * kMaxShapes);
+    tab.T = E.d_T.as<double>((size_t)nrows * n_req);
+    tab.O = E.d_O.as<double>((size_t)nrows * n_req);
+    {
+        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
+        double* dL = E.d_crn.as<double>(L.size());
+        x.h2d(dL, L.data(), L.size() * sizeof(double));
+        RowSetupArgs ra;
+        ra.nrows = nrows;
+        ra.n_req = n_req;
+        ra.rows = static_cast<RowDesc*>(E.d_rows.p);
+        ra.spaces = static_cast<PlanSpace*>(E.d_spaces.p);
+        ra.models = static_cast<ModelArgs*>(E.d_models.p);
+        ra.hw = {hw.flops_per_gpu, hw.mem_bandwidth_per_gpu, hw.mem_capacity_per_gpu};
+        ra.p = {q.prefill_efficiency, q.decode_bw_efficiency, q.pipeline_bubble_factor,
+                q.comm_overhead_per_stage, q.kv_memory_fraction};
+        ra.tab = tab;
+        launch_row_setup(ra, dL, x.s, &x.launches);
+    }
+
+    unsigned long long* latmin = E.d_latmin.as<unsigned long long>(cells);
+    unsigned long long* ub = E.d_ub.as<unsigned long long>(cells);
+    x.fill(latmin, cells, kInfBits);
+    x.fill(ub, cells, kInfBits);
+    TieEntry* ties = E.d_ties.as<TieEntry>(E.tie_cap);
+    unsigned long long* tiecnt = E.d_tiecnt.as<unsigned long long>(1);
+    SimItem* ovf = E.d_ovf.as<SimItem>(E.ovf_cap);
+    unsigned long long* ovfcnt = E.d_ovfcnt.as<unsigned long long>(1);
+    unsigned long long* ovfcnt2 = E.d_ovfcnt2.as<unsigned long long>(1);
+    unsigned long long* ctrs = E.d_ctrs.as<unsigned long long>(CTR_COUNT);
+    unsigned long long* ictr = E.d_ictr.as<unsigned long long>(1);
+    CG_CUDA(cudaMemsetAsync(tiecnt, 0, 8, x.s));
+    CG_CUDA(cudaMemsetAsync(ctrs, 0, 8 * CTR_COUNT, x.s));
+
+    const int K = n_req - (int)p95_index(n_req);
+    std::map<int, std::vector<int>> by_cls;
+    for (int r = 0; r < nrows; ++r) {
+        const auto& sp = hs[rows[r].space];
+        x.st.plans_enumerated += (long long)sp.num_plans;
+        if (sp.num_plans == 0 || N < 1) continue;
+        by_cls[rows[r].cls].push_back(r);
+    }
+    long long max_slots = 1;
+    for (auto& kv : by_cls) {
+        SimGeometry g = sim_geometry(kv.first, false, E.sm_count);
+        SimGeometry gd = sim_geometry(kv.first, true, E.sm_count);
+        max_slots = std::max({max_slots, g.slots, gd.slots});
+    }
+    double* scratch = E.d_scratch.as<double>((size_t)max_slots * n_req);
+    int ring_cap = 1;
+    while (ring_cap < n_req) ring_cap <<= 1;
+
+    CG_CUDA(cudaEventRecord(E.ev[8], x.s));
+    for (auto& kv : by_cls) {
+        const int cls = kv.first;
+        const auto& rl = kv.second;
+        std::vector<unsigned long long> prefix(rl.size() + 1, 0);
+        for (size_t i = 0; i < rl.size(); ++i) {
+            const unsigned long long P = hs[rows[rl[i]].space].num_plans;
+            prefix[i + 1] = prefix[i] + (P + E.item_plans - 1) / E.item_plans;
+        }
+        const unsigned long long total_items = prefix.back();
+        const unsigned long long lo = total_items * (unsigned long long)E.rank / (unsigned long long)E.world;
+        const unsigned long long hi =
+            total_items * (unsigned long long)(E.rank + 1) / (unsigned long long)E.world;
+        int* rowids = E.d_rowids.as<int>(rl.size());
+        unsigned long long* ipre = E.d_iprefix.as<unsigned long long>(prefix.size());
+        x.h2d(rowids, rl.data(), rl.size() * sizeof(int));
+        x.h2d(ipre, prefix.data(), prefix.size() * sizeof(unsigned long long));
+        x.h2d(ictr, &lo, 8);
+        CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
+
+        SimArgs a{};
+        a.N = N;
+        a.n_req = n_req;
+        a.K = K;
+        a.prune = E.prune;
+        a.item_plans = E.item_plans;
+        a.nrows = (int)rl.size();
+        a.row_ids = rowids;
+        a.item_prefix = ipre;
+        a.nitems = hi;
+        a.item_counter = ictr;
+        a.rows = static_cast<RowDesc*>(E.d_rows.p);
+        a.spaces = static_cast<PlanSpace*>(E.d_spaces.p);
+        a.tab = tab;
+        a.lat_min = latmin;
+        a.ub = ub;
+        a.ties = ties;
+        a.tie_count = tiecnt;
+        a.tie_cap = (unsigned long long)E.tie_cap;
+        a.ovf = ovf;
+        a.ovf_count = ovfcnt;
+        a.ovf_cap = (unsigned long long)E.ovf_cap;
+        a.scratch = scratch;
+        a.counters = ctrs;
+        a.ring_cap = ring_cap;
+        if (hi > lo) launch_sim(a, cls, false, E.sm_count, x.s, &x.launches, nullptr);
+        unsigned long long novf = 0;
+        x.d2h(&novf, ovfcnt, 8);
+        x.sync();
+        if (novf > (unsigned long long)E.ovf_cap) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
+        x.st.plans_overflow += (long long)novf;
+        if (novf > 0) {  // deep-queue re-runs (rings in global memory, capacity >= n_req)
+            SimGeometry gd = sim_geometry(cls, true, E.sm_count);
+            double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
+            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
+            CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
+            SimArgs d = a;
+            d.deep_items = ovf;
+            d.nitems = novf;
+            d.ring_global = ring;
+            d.ovf_count = ovfcnt2;
+            launch_sim(d, cls, true, E.sm_count, x.s, &x.launches, nullptr);
+        }
+    }
+    CG_CUDA(cudaEventRecord(E.ev[9], x.s));
+
+    unsigned long long h_ctr[CTR_COUNT], h_ties = 0;
+    x.d2h(h_ctr, ctrs, sizeof(h_ctr));
+    x.d2h(&h_ties, tiecnt, 8);
+    x.sync();
+    float k4ms = 0;
+    CG_CUDA(cudaEventElapsedTime(&k4ms, E.ev[8], E.ev[9]));
+    x.st.ms_k4 += k4ms;
+    if (h_ties > (unsigned long long)E.tie_cap) fail(CG_ERR_CUDA, "tie list exhausted");
+    x.st.plans_stable += (long long)h_ctr[CTR_STABLE];
+    x.st.plans_simulated_full += (long long)h_ctr[CTR_FULL];
+    x.st.plans_pruned += (long long)h_ctr[CTR_PRUNED];
+    x.st.request_steps += (long long)h_ctr[CTR_STEPS];
+
+    unsigned long long* best = E.d_best.as<unsigned long long>(cells);
+    x.fill(best, cells, ~0ull);
+    ResolveArgs ra;
+    ra.N = N;
+    ra.nrows = nrows;
+    ra.nties = h_ties;
+    ra.ties = ties;
+    ra.rows = static_cast<RowDesc*>(E.d_rows.p);
+    ra.spaces = static_cast<PlanSpace*>(E.d_spaces.p);
+    ra.lat_min = latmin;
+    ra.best_plan = best;
+    ra.final_lat = E.d_flat.as<double>(cells);
+    ra.final_plan = E.d_fplan.as<long long>(cells);
+    if (E.world > 1) {
+        // resolve ties locally, exchange (lat_min, best) with one all-gather, merge
+        ResolveArgs local = ra;
+        local.nrows = 0;
+        launch_resolve(local, x.s, &x.launches);
+        unsigned long long* send = E.d_send.as<unsigned long long>((size_t)cells * 2);
+        unsigned long long* gathered = E.d_gather.as<unsigned long long>((size_t)cells * 2 * E.world);
+        CG_CUDA(cudaMemcpyAsync(send, latmin, cells * 8, cudaMemcpyDeviceToDevice, x.s));
+        CG_CUDA(cudaMemcpyAsync(send + cells, best, cells * 8, cudaMemcpyDeviceToDevice, x.s));
+        x.sync();
+        if (!E.allgather || E.allgather(send, gathered, (size_t)cells * 16, E.ag_user) != 0)
+            fail(CG_ERR_CUDA, "all-gather callback failed");
+        k_merge_ranks<<<(unsigned)((cells + 127) / 128), 128, 0, x.s>>>(gathered, E.world, cells, N, ra.rows,
+                                                                       ra.spaces, latmin, best);
+        CG_LAUNCH_CHECK();
+        ++x.launches;
+        ra.nties = 0;
+    }
+    launch_resolve(ra, x.s, &x.launches);
+}
+
+// ParallelismPlan expansion of plan index p in space sp (canonical order).
+void expand_plan(const HostPlanSpace& sp, long long p, std::vector<cg_replica>& reps, cg_plan& out) {
+    std::vector<int> c;
+    sp.unrank((unsigned long long)p, c);
+    out.replica_offset = (int64_t)reps.size();
+    out.gpus_used = 0;
+    out.dp = 0;
+    for (size_t s = 0; s < c.size(); ++s)
+        for (int k = 0; k < c[s]; ++k) {
+            reps.push_back({sp.shapes[s].tp, sp.shapes[s].pp});
+            out.gpus_used += sp.shapes[s].gpus;
+            out.dp += 1;
+        }
+}
+
+template <class T>
+T* hcopy(const std::vector<T>& v) {
+    T* p = static_cast<T*>(std::malloc(sizeof(T) * (v.empty() ? 1 : v.size())));
+    if (!p) throw std::bad_alloc();
+    if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+    return p;
+}
+
+struct WlKey {
+    int stage;
+    unsigned long long b[5];
+    bool operator==(const WlKey& o) const {
+        return stage == o.stage && std::memcmp(b, o.b, sizeof(b)) == 0;
+    }
+};
+struct WlKeyHash {
+    size_t operator()(const WlKey& k) const {
+        unsigned long long h = 1469598103934665603ull ^ (unsigned long long)k.stage;
+        for (auto v : k.b) {
+            h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+            h *= 1099511628211ull;
+        }
+        return (size_t)h;
+    }
+};
+
+// Trace columns in HBM (copied when the caller passed host pointers).
+struct TraceDev {
+    long long n;
+    int C;
+    const double *scores, *in, *out;
+    double first_arrival, last_arrival;
+};
+
+TraceDev trace_to_device(SweepCtx& x, const cg_trace& tr) {
+    TraceDev t{};
+    t.n = tr.n;
+    t.C = tr.stages;
+    const size_t n = (size_t)tr.n;
+    if (tr.on_device) {
+        t.scores = tr.scores;
+        t.in = tr.input_tokens;
+        t.out = tr.output_tokens;
+        if (n >= 1) {
+            x.d2h(&t.first_arrival, tr.arrival_s, 8);
+            x.d2h(&t.last_arrival, tr.arrival_s + n - 1, 8);
+            x.sync();
+        }
+    } else {
+        double* s = x.E.d_scores.as<double>(n * tr.stages);
+        double* in = x.E.d_in.as<double>(n);
+        double* out = x.E.d_out.as<double>(n * tr.stages);
+        x.h2d(s, tr.scores, n * tr.stages * sizeof(double));
+        x.h2d(in, tr.input_tokens, n * sizeof(double));
+        x.h2d(out, tr.output_tokens, n * tr.stages * sizeof(double));
+        t.scores = s;
+        t.in = in;
+        t.out = out;
+        if (n >= 1) {
+            t.first_arrival = tr.arrival_s[0];
+            t.last_arrival = tr.arrival_s[n - 1];
+        }
+    }
+    return t;
+}
+
+// overall_arrival_rate (domain.cpp:396-401)
+double overall_rate(const TraceDev& t) {
+    if (t.n < 2) return 0.0;
+    const double span = t.last_arrival - t.first_arrival;
+    if (span <= 0.0) return 0.0;
+    return static_cast<double>(t.n) / span;
+}
+
+// default_threshold_grid (outerplan.cpp:114-132) with GPU-sorted scores.
+std::vector<std::vector<double>> default_grid(SweepCtx& x, const TraceDev& t) {
+    std::vector<std::vector<double>> grid;
+    const long long n = t.n;
+    cg_engine& E = x.E;
+    for (int d = 0; d + 1 < t.C; ++d) {
+        unsigned long long* k0 = E.d_lk0.as<unsigned long long>(n);
+        unsigned long long* k1 = E.d_lk1.as<unsigned long long>(n);
+        unsigned int* hist = E.d_rshist.as<unsigned int>(radix_hist_entries(n));
+        unsigned long long* orax = E.d_orax.as<unsigned long long>(2);
+        k_score_keys<<<(unsigned)((n + 255) / 256), 256, 0, x.s>>>(t.scores + (long long)d * n, n, k0);
+        CG_LAUNCH_CHECK();
+        ++x.launches;
+        launch_or_and(k0, n, orax, x.s, &x.launches);
+        unsigned long long h[2];
+        x.d2h(h, orax, sizeof(h));
+        x.sync();
+        const int par = radix_sort_u64(k0, nullptr, k1, nullptr, n, h[0] ^ h[1], hist, x.s, &x.launches);
+        const unsigned long long* sorted = par ? k1 : k0;
+        std::vector<double> values{0.0, kThresholdSentinel};
+        std::vector<unsigned long long> keys(9);
+        for (int q = 1; q <= 9; ++q) {
+            const double qq = q / 10.0;
+            auto rank = static_cast<long long>(std::ceil(qq * static_cast<double>(n)));
+            rank = std::clamp<long long>(rank, 1, n);
+            x.d2h(&keys[q - 1], sorted + (rank - 1), 8);
+        }
+        x.sync();
+        for (auto k : keys) values.push_back(key_to_dbl(k));
+        std::sort(values.begin(), values.end());
+        values.erase(std::unique(values.begin(), values.end()), values.end());
+        grid.push_back(std::move(values));
+    }
+    return grid;
+}
+
+struct RoutingOut {
+    int C = 0, D = 0;
+    long long n = 0;
+    std::vector<int> G;                  // distinct per dim
+    std::vector<long long> P;            // workloads per stage
+    std::vector<long long> off;          // workload offsets per stage (C+1)
+    long long total = 0;
+    long long ntuples = 0;
+    std::vector<double> stats;           // [total][5]
+    std::vector<unsigned long long> count;
+    double z2_qsum = 0;                  // all-forward score sum
+    bool integral = true;
+};
+
+// K1-K3 + K2 for distinct sorted grids (one value list per dim).
+RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vector<double>>& distinct,
+                     double rate, const std::vector<double>* extra_thresholds) {
+    cg_engine& E = x.E;
+    RoutingOut R;
+    R.C = t.C;
+    R.D = t.C - 1;
+    R.n = t.n;
+    const long long n = t.n;
+    const int C = t.C, D = R.D;
+    const int Q = 2 + C;
+    RouteArgs ra{};
+    ra.n = n;
+    ra.scores = t.scores;
+    ra.in = t.in;
+    ra.out = t.out;
+    std::vector<double> gv;
+    long long cells = 1;
+    for (int d = 0; d < D; ++d) {
+        const int g = (int)distinct[d].size();
+        if (g > 65534) fail(CG_ERR_UNSUPPORTED, "more than 65534 distinct thresholds in a grid dimension");
+        R.G.push_back(g);
+        ra.goff[d] = (int)gv.size();
+        ra.G[d] = g;
+        ra.stride[d] = cells;
+        cells *= (g + 1);
+        if (cells > (1LL << 31)) fail(CG_ERR_UNSUPPORTED, "threshold grid too large for the rank histogram");
+        gv.insert(gv.end(), distinct[d].begin(), distinct[d].end());
+    }
+    ra.gtotal = (int)gv.size();
+    ra.grid_in_smem = ra.gtotal <= 6144 ? 1 : 0;
+    double* dgv = E.d_gvals.as<double>(std::max<size_t>(1, gv.size()));
+    x.h2d(dgv, gv.data(), gv.size() * sizeof(double));
+    ra.gvals = dgv;
+    ra.ranks = E.d_ranks.as<unsigned long long>(n);
+    ra.hist = E.d_hist.as<unsigned long long>((size_t)cells * Q);
+    ra.flags = E.d_flags.as<unsigned int>(1);
+    CG_CUDA(cudaMemsetAsync(ra.hist, 0, (size_t)cells * Q * 8, x.s));
+    CG_CUDA(cudaMemsetAsync(ra.flags, 0, 4, x.s));
+
+    CG_CUDA(cudaEventRecord(E.ev[0], x.s));
+    launch_route_aggregate(ra, D, E.sm_count, x.s, &x.launches);
+    CG_CUDA(cudaEventRecord(E.ev[1], x.s));
+    launch_hist_scan(ra.hist, cells, Q, ra.stride, ra.G, D, x.s, &x.launches);
+
+    // workloads per (stage, prefix)
+    R.P.assign(C, 1);
+    R.off.assign(C + 1, 0);
+    for (int i = 0; i < C; ++i) {
+        long long p = 1;
+        for (int d = 0; d < i; ++d) p *= R.G[d];
+        R.P[i] = p;
+        R.off[i + 1] = R.off[i] + p;
+    }
+    R.total = R.off[C];
+    R.ntuples = R.P[C - 1];
+    WorkloadArgs wa{};
+    wa.C = C;
+    wa.total = R.total;
+    for (int i = 0; i <= C; ++i) wa.wl_off[i] = R.off[i];
+    for (int d = 0; d < D; ++d) {
+        wa.G[d] = R.G[d];
+        wa.stride[d] = ra.stride[d];
+    }
+    wa.hist = ra.hist;
+    wa.count = E.d_wcount.as<unsigned long long>(R.total);
+    wa.sum_in = E.d_wsin.as<unsigned long long>(R.total);
+    wa.sum_out = E.d_wsout.as<unsigned long long>(R.total);
+    launch_workload_counts(wa, x.s, &x.launches);
+
+    // sorted token columns for the p95 scans
+    const int L = C + 1;
+    unsigned long long* lk0 = E.d_lk0.as<unsigned long long>((size_t)L * n);
+    unsigned long long* lv0 = E.d_lv0.as<unsigned long long>((size_t)L * n);
+    unsigned long long* lk1 = E.d_lk1.as<unsigned long long>((size_t)L * n);
+    unsigned long long* lv1 = E.d_lv1.as<unsigned long long>((size_t)L * n);
+    unsigned int* rshist = E.d_rshist.as<unsigned int>(radix_hist_entries(n));
+    unsigned long long* orax = E.d_orax.as<unsigned long long>(2 * L + Q);
+    launch_make_lists(t.in, t.out, ra.ranks, n, C, lk0, lv0, E.sm_count, x.s, &x.launches);
+    for (int l = 0; l < L; ++l) launch_or_and(lk0 + (long long)l * n, n, orax + 2 * l, x.s, &x.launches);
+    // totals of the full histogram cell (sums over the whole trace)
+    CG_CUDA(cudaMemcpyAsync(orax + 2 * L, ra.hist + (cells - 1) * Q, Q * 8, cudaMemcpyDeviceToDevice, x.s));
+    std::vector<unsigned long long> h_orax(2 * L + Q);
+    unsigned int h_flags = 0;
+    x.d2h(h_orax.data(), orax, h_orax.size() * 8);
+    x.d2h(&h_flags, ra.flags, 4);
+    x.sync();
+    unsigned long long varying = 0;
+    for (int l = 0; l < L; ++l) varying |= h_orax[2 * l] ^ h_orax[2 * l + 1];
+    R.integral = (h_flags & 1u) == 0;
+    for (int q = 1; q < Q; ++q)
+        if (h_orax[2 * L + q] >= (1ull << 53)) R.integral = false;
+    int par = 0;
+    for (int l = 0; l < L; ++l)
+        par = radix_sort_u64(lk0 + (long long)l * n, lv0 + (long long)l * n, lk1 + (long long)l * n,
+                             lv1 + (long long)l * n, n, varying, rshist, x.s, &x.launches);
+    const unsigned long long* sk = par ? lk1 : lk0;
+    const unsigned long long* sv = par ? lv1 : lv0;
+    double* p95i = E.d_wp95i.as<double>(R.total);
+    double* p95o = E.d_wp95o.as<double>(R.total);
+    launch_p95_scan(wa, sk, sv, n, p95i, p95o, x.s, &x.launches);
+    double* sinf = E.d_wsinf.as<double>(R.total);
+    double* soutf = E.d_wsoutf.as<double>(R.total);
+    if (!R.integral)
+        launch_workload_seq_sums(wa, ra.ranks, t.in, t.out, n, sinf, soutf, x.s, &x.launches);
+    double* stats = E.d_wstats.as<double>((size_t)R.total * 5);
+    launch_workload_stats(wa, n, rate, R.integral ? 1 : 0, sinf, soutf, p95i, p95o, stats, x.s, &x.launches);
+    CG_CUDA(cudaEventRecord(E.ev[2], x.s));
+
+    // K2: quality for every distinct tuple (+ optional extra threshold rows)
+    const long long extra = extra_thresholds ? (long long)(extra_thresholds->size() / std::max(1, D)) : 0;
+    const long long nq = R.ntuples + (extra_thresholds ? (D > 0 ? extra : 1) : 0);
+    std::vector<double> thr((size_t)std::max(1LL, nq * D));
+    for (long long tu = 0; tu < R.ntuples; ++tu) {
+        long long w = tu;
+        for (int d = 0; d < D; ++d) {
+            thr[(size_t)tu * D + d] = distinct[d][w % R.G[d]];
+            w /= R.G[d];
+        }
+    }
+    if (extra_thresholds && D > 0)
+        std::copy(extra_thresholds->begin(), extra_thresholds->end(), thr.begin() + (size_t)R.ntuples * D);
+    double* dthr = E.d_thr.as<double>(thr.size());
+    x.h2d(dthr, thr.data(), (size_t)nq * D * sizeof(double));
+    double* qsum = E.d_qsum.as<double>(nq);
+    launch_quality(t.scores, n, D, dthr, nq, qsum, x.s, &x.launches);
+    CG_CUDA(cudaEventRecord(E.ev[3], x.s));
+
+    R.stats.resize((size_t)R.total * 5);
+    R.count.resize(R.total);
+    x.d2h(R.stats.data(), stats, R.stats.size() * 8);
+    x.d2h(R.count.data(), wa.count, R.count.size() * 8);
+    if (extra_thresholds) x.d2h(&R.z2_qsum, qsum + R.ntuples, 8);
+    x.sync();
+    float m_k1 = 0, m_route = 0, m_q = 0;
+    CG_CUDA(cudaEventElapsedTime(&m_k1, E.ev[0], E.ev[1]));
+    CG_CUDA(cudaEventElapsedTime(&m_route, E.ev[0], E.ev[2]));
+    CG_CUDA(cudaEventElapsedTime(&m_q, E.ev[2], E.ev[3]));
+    x.st.ms_k1 += m_k1;
+    x.st.k1_bytes += (double)n * (8.0 * (D + 1 + C) + 8.0);
+    x.st.ms_route += m_route;
+    x.st.ms_quality += m_q;
+    x.st.stage_workloads += R.total;
+    return R;
+}
+
+void free_result(cg_sweep_result* r) {
+    if (!r) return;
+    std::free(r->eval_candidate);
+    std::free(r->eval_thresholds);
+    std::free(r->eval_latency);
+    std::free(r->eval_quality);
+    std::free(r->eval_ratios);
+    std::free(r->eval_allocations);
+    std::free(r->eval_plan);
+    std::free(r->plans);
+    std::free(r->replicas);
+    std::free(r->weights);
+    std::free(r->weight_selection);
+    std::free(r->front);
+    std::free(r->skipped_candidate);
+    std::free(r->skipped_thresholds);
+    std::free(r);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char* cg_version(void) { return "cascade-gpu 0.1 (sm_100a)"; }
+
+cg_status cg_engine_create(int32_t device, cg_engine** out) {
+    return guarded([&] {
+        *out = nullptr;
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            fail(CG_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+        if (device < 0 || device >= n) fail(CG_ERR_CUDA, "invalid CUDA device ordinal");
+        CG_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CG_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10) fail(CG_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 class");
+        auto* e = new cg_engine();
+        e->device = device;
+        e->sm_count = prop.multiProcessorCount;
+        CG_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+        for (auto& ev : e->ev) CG_CUDA(cudaEventCreate(&ev));
+        *out = e;
+    });
+}
+
+void cg_engine_destroy(cg_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    for (auto& ev : e->ev) cudaEventDestroy(ev);
+    if (e->s) cudaStreamDestroy(e->s);
+    delete e;
+}
+
+cg_status cg_engine_set_collective(cg_engine* e, int32_t rank, int32_t world, cg_allgather_fn fn, void* user) {
+    return guarded([&] {
+        if (!e) fail(CG_ERR_INVALID_INPUT, "null engine");
+        if (world < 1 || rank < 0 || rank >= world) fail(CG_ERR_INVALID_INPUT, "invalid rank/world");
+        if (world > 1 && !fn) fail(CG_ERR_INVALID_INPUT, "multi-rank engine needs an all-gather callback");
+        e->rank = rank;
+        e->world = world;
+        e->allgather = fn;
+        e->ag_user = user;
+    });
+}
+
+cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
+    return guarded([&] {
+        if (!e || !key) fail(CG_ERR_INVALID_INPUT, "null engine/key");
+        const std::string k(key);
+        if (k == "prune") e->prune = value ? 1 : 0;
+        else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
+        else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
+        else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);
+        else fail(CG_ERR_INVALID_INPUT, "unknown option " + k);
+    });
+}
+
+cg_status cg_sweep(cg_engine* E, const cg_trace* tr, const cg_model* models, int32_t C, const cg_hardware* hw,
+                   const cg_cost_params* q, int32_t total_gpus, const cg_sweep_config* cfg,
+                   cg_sweep_result** out) {
+    return guarded([&] {
+        Timer timer;
+        if (out) *out = nullptr;
+        if (!E || !tr || !hw || !q || !cfg || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        CG_CUDA(cudaSetDevice(E->device));
+        SweepCtx x(*E);
+
+        // ---- validation in the reference order (outerplan.cpp:170-189)
+        if (tr->n <= 0) fail(CG_ERR_EMPTY_TRACE, "sweep: empty trace");
+        validate_models(models, C);
+        if (C > kMaxStages) fail(CG_ERR_UNSUPPORTED, "GPU engine supports up to 5 cascade stages");
+        TraceDev t = trace_to_device(x, *tr);
+        const double rate = overall_rate(t);
+        if (rate <= 0.0) fail(CG_ERR_INVALID_INPUT, "sweep: trace has no positive arrival-rate span");
+        if (tr->stages != C) fail(CG_ERR_INVALID_INPUT, "sweep: trace record stage count != C");
+        const int D = C - 1;
+
+        std::vector<std::vector<double>> given;
+        if (cfg->grid_dims == 0) {
+            given = default_grid(x, t);
+        } else {
+            long long off = 0;
+            for (int d = 0; d < cfg->grid_dims; ++d) {
+                given.emplace_back(cfg->grid_values + off, cfg->grid_values + off + cfg->grid_sizes[d]);
+                off += cfg->grid_sizes[d];
+            }
+        }
+        if ((int)given.size() != D) fail(CG_ERR_INVALID_INPUT, "sweep: threshold grid must have C-1 dimensions");
+        for (const auto& dim : given)
+            if (dim.empty()) fail(CG_ERR_INVALID_INPUT, "sweep: empty threshold grid dimension");
+        // StageEvaluator constructor (costmodel.cpp:199-203)
+        validate_hw(*hw);
+        validate_params(*q);
+
+        std::vector<std::vector<double>> distinct(D);
+        std::vector<std::vector<int>> g2d(D);
+        for (int d = 0; d < D; ++d) {
+            distinct[d] = given[d];
+            std::sort(distinct[d].begin(), distinct[d].end());
+            distinct[d].erase(std::unique(distinct[d].begin(), distinct[d].end()), distinct[d].end());
+            for (double v : given[d])
+                g2d[d].push_back(
+                    (int)(std::lower_bound(distinct[d].begin(), distinct[d].end(), v) - distinct[d].begin()));
+        }
+        long long ncand = 1;
+        for (int d = 0; d < D; ++d) ncand *= (long long)given[d].size();
+        x.st.candidates = ncand;
+
+        // ---- routing of every workload + quality of every tuple (+ all-forward for z2*)
+        std::vector<double> allfwd((size_t)std::max(1, D), kThresholdSentinel);
+        RoutingOut R = route_all(x, t, distinct, rate, &allfwd);
+        x.st.distinct_candidates = R.ntuples;
+
+        // ---- row cache: validation in candidate order, exact-bit dedup
+        const int N = total_gpus;
+        if (N < 0) fail(CG_ERR_INVALID_INPUT, "sweep: total_gpus must be >= 0");
+        std::string w0 = workload_problems(&R.stats[0]);
+        if (!w0.empty()) fail(CG_ERR_INVALID_INPUT, w0);
+        std::vector<char> invalid(R.total, 0);
+        bool any_invalid = false;
+        for (long long w = 0; w < R.total; ++w)
+            if (R.count[w] > 0 && !workload_problems(&R.stats[(size_t)w * 5]).empty()) {
+                invalid[w] = 1;
+                any_invalid = true;
+            }
+        auto hs = build_spaces(x, models, C, *hw, *q, N);
+        std::vector<int> wl_row(R.total, -1);
+        std::vector<RowDesc> rows;
+        std::unordered_map<WlKey, int, WlKeyHash> cache;
+        for (int i = 0; i < C; ++i) {
+            for (long long w = R.off[i]; w < R.off[i + 1]; ++w) {
+                if (R.count[w] == 0 || invalid[w]) continue;
+                if (any_invalid && w != 0) continue;  // only the utopia row is evaluated
+                WlKey key{};
+                key.stage = i;
+                std::memcpy(key.b, &R.stats[(size_t)w * 5], 40);
+                auto it = cache.find(key);
+                if (it != cache.end()) {
+                    wl_row[w] = it->second;
+                    continue;
+                }
+                RowDesc rd{};
+                rd.stage = i;
+                rd.space = i;
+                rd.cls = row_class(hs[i], N);
+                rd.dpmax = hs[i].min_gpus > 0 ? N / hs[i].min_gpus : 0;
+                rd.rate = R.stats[(size_t)w * 5 + 0];
+                rd.mean_in = R.stats[(size_t)w * 5 + 1];
+                rd.mean_out = R.stats[(size_t)w * 5 + 2];
+                rd.p95_in = R.stats[(size_t)w * 5 + 3];
+                rd.p95_out = R.stats[(size_t)w * 5 + 4];
+                const int id = (int)rows.size();
+                rows.push_back(rd);
+                cache.emplace(key, id);
+                wl_row[w] = id;
+            }
+        }
+        x.st.unique_rows = (long long)rows.size();
+
+        CG_CUDA(cudaEventRecord(E->ev[4], x.s));
+        evaluate_rows(x, rows, hs, *hw, *q, N);
+        CG_CUDA(cudaEventRecord(E->ev[5], x.s));
+
+        // utopia (outerplan.cpp:206-219)
+        double z1 = dinf();
+        x.d2h(&z1, static_cast<double*>(E->d_flat.p) + (size_t)wl_row[0] * (N + 1) + N, 8);
+        x.sync();
+        if (std::isinf(z1)) fail(CG_ERR_INFEASIBLE, "smallest model cannot be served within the budget");
+        const double z2 = R.z2_qsum / static_cast<double>(t.n);
+        if (any_invalid) {
+            // first live invalid workload in candidate order (the reference's throw point)
+            for (long long c = 0; c < ncand; ++c) {
+                long long rem = c, tuple = 0, ts = 1;
+                std::vector<int> gi(D);
+                for (int d = D - 1; d >= 0; --d) {
+                    gi[d] = (int)(rem % (long long)given[d].size());
+                    rem /= (long long)given[d].size();
+                }
+                for (int d = 0; d < D; ++d) {
+                    tuple += (long long)g2d[d][gi[d]] * ts;
+                    ts *= R.G[d];
+                }
+                for (int i = 0; i < C; ++i) {
+                    const long long w = R.off[i] + (i == 0 ? 0 : tuple % R.P[i]);
+                    if (R.count[w] > 0 && invalid[w]) fail(CG_ERR_INVALID_INPUT, workload_problems(&R.stats[(size_t)w * 5]));
+                }
+            }
+        }
+
+        // ---- K6: min-max solve per distinct tuple
+        int* dwlrow = E->d_wlrow.as<int>(R.total);
+        x.h2d(dwlrow, wl_row.data(), wl_row.size() * sizeof(int));
+        SolveArgs sa{};
+        sa.C = C;
+        sa.N = N;
+        sa.total_gpus = N;
+        sa.raw_f0 = 0;
+        sa.ntuples = R.ntuples;
+        for (int i = 0; i <= C; ++i) sa.wl_off[i] = R.off[i];
+        for (int i = 0; i < C; ++i) sa.wl_P[i] = R.P[i];
+        sa.wl_count = static_cast<unsigned long long*>(E->d_wcount.p);
+        sa.wl_row = dwlrow;
+        sa.final_lat = static_cast<double*>(E->d_flat.p);
+        sa.final_plan = static_cast<long long*>(E->d_fplan.p);
+        sa.feasible = E->d_tfeas.as<unsigned char>(R.ntuples);
+        sa.L = E->d_tL.as<double>(R.ntuples);
+        sa.alloc = E->d_talloc.as<int>((size_t)R.ntuples * C);
+        sa.plan = E->d_tplan.as<long long>((size_t)R.ntuples * C);
+        launch_solve(sa, x.s, &x.launches);
+
+        // ---- grid-order expansion, compaction into evaluations / skipped
+        ExpandArgs ea{};
+        ea.D = D;
+        ea.ncand = ncand;
+        std::vector<int> g2d_flat;
+        for (int d = 0; d < D; ++d) {
+            ea.Gg[d] = (int)given[d].size();
+            ea.Gd[d] = R.G[d];
+            ea.goff[d] = (int)g2d_flat.size();
+            g2d_flat.insert(g2d_flat.end(), g2d[d].begin(), g2d[d].end());
+        }
+        int* dg2d = E->d_g2d.as<int>(std::max<size_t>(1, g2d_flat.size()));
+        x.h2d(dg2d, g2d_flat.data(), g2d_flat.size() * sizeof(int));
+        ea.g2d = dg2d;
+        ea.tuple_feasible = sa.feasible;
+        ea.cand_tuple = E->d_ctuple.as<long long>(ncand);
+        ea.flag = E->d_cflag.as<unsigned>(ncand);
+        unsigned* pos = E->d_pos.as<unsigned>(ncand);
+        unsigned long long* total = E->d_total.as<unsigned long long>(1);
+        long long* ecand = E->d_ecand.as<long long>(ncand);
+        double* eL = E->d_eL.as<double>(ncand);
+        double* eQ = E->d_eQ.as<double>(ncand);
+        long long* skip = E->d_skip.as<long long>(ncand);
+        double* qsum = static_cast<double*>(E->d_qsum.p);
+        launch_expand(ea, pos, total, sa.L, qsum, static_cast<double>(t.n), ecand, eL, eQ, skip, x.s, &x.launches);
+        unsigned long long h_total = 0;
+        x.d2h(&h_total, total, 8);
+        x.sync();
+        const long long nE = (long long)h_total;
+        if (nE == 0) fail(CG_ERR_INFEASIBLE_PROBLEM, "sweep: every threshold candidate is infeasible");
+        auto weights = weight_ladder(cfg->weight_ratio_min, cfg->weight_ratio_max, cfg->weight_count);
+        const int nw = (int)weights.size() / 2;
+
+        // ---- K7: Tchebycheff per weight + Pareto front
+        double* dw = E->d_weights.as<double>(weights.size());
+        x.h2d(dw, weights.data(), weights.size() * sizeof(double));
+        int* sel = E->d_sel.as<int>(nw);
+        launch_tchebycheff(eL, eQ, nE, dw, nw, z1, z2, sel, x.s, &x.launches);
+        long long* front = E->d_front.as<long long>(nE);
+        long long* fsize = E->d_fsize.as<long long>(1);
+        launch_pareto(eL, eQ, nE, E->d_pk0.as<unsigned long long>(nE), E->d_pk1.as<unsigned long long>(nE),
+                      E->d_pv0.as<unsigned long long>(nE), E->d_pv1.as<unsigned long long>(nE),
+                      E->d_pkl.as<unsigned long long>(nE), E->d_orax.as<unsigned long long>(2),
+                      E->d_rshist.as<unsigned int>(radix_hist_entries(nE)), front, fsize, x.s, &x.launches);
+        CG_CUDA(cudaEventRecord(E->ev[6], x.s));
+
+        // ---- results to host
+        std::vector<long long> h_ecand(nE), h_ctuple(ncand), h_front, h_skip(ncand - nE);
+        std::vector<double> h_eL(nE), h_eQ(nE);
+        std::vector<int> h_sel(nw), h_alloc((size_t)R.ntuples * C);
+        std::vector<long long> h_plan((size_t)R.ntuples * C);
+        long long h_fsize = 0;
+        x.d2h(h_ecand.data(), ecand, nE * 8);
+        x.d2h(h_eL.data(), eL, nE * 8);
+        x.d2h(h_eQ.data(), eQ, nE * 8);
+        x.d2h(h_ctuple.data(), ea.cand_tuple, ncand * 8);
+        x.d2h(h_skip.data(), skip, (ncand - nE) * 8);
+        x.d2h(h_sel.data(), sel, nw * 4);
+        x.d2h(h_alloc.data(), sa.alloc, h_alloc.size() * 4);
+        x.d2h(h_plan.data(), sa.plan, h_plan.size() * 8);
+        x.d2h(&h_fsize, fsize, 8);
+        x.sync();
+        h_front.resize(h_fsize);
+        x.d2h(h_front.data(), front, h_fsize * 8);
+        x.sync();
+        float m_rows = 0, m_solve = 0;
+        CG_CUDA(cudaEventElapsedTime(&m_rows, E->ev[4], E->ev[5]));
+        CG_CUDA(cudaEventElapsedTime(&m_solve, E->ev[5], E->ev[6]));
+        x.st.ms_rows += m_rows;
+        x.st.ms_solve += m_solve;
+
+        // ---- assemble SweepResult
+        auto* r = static_cast<cg_sweep_result*>(std::calloc(1, sizeof(cg_sweep_result)));
+        if (!r) throw std::bad_alloc();
+        try {
+            r->stages = C;
+            r->z1_star = z1;
+            r->z2_star = z2;
+            r->num_evaluations = nE;
+            std::vector<double> thr((size_t)nE * D), ratios((size_t)nE * C);
+            std::vector<int32_t> alloc((size_t)nE * C);
+            std::vector<int64_t> eplan((size_t)nE * C, -1);
+            std::vector<cg_plan> plans;
+            std::vector<cg_replica> reps;
+            std::map<std::pair<int, long long>, int64_t> plan_ids;
+            auto decode_thresholds = [&](long long c, double* dst) {
+                long long rem = c;
+                for (int d = D - 1; d >= 0; --d) {
+                    const long long gi = rem % (long long)given[d].size();
+                    rem /= (long long)given[d].size();
+                    dst[d] = given[d][gi];
+                }
+            };
+            for (long long e = 0; e < nE; ++e) {
+                const long long c = h_ecand[e];
+                const long long tu = h_ctuple[c];
+                decode_thresholds(c, thr.data() + (size_t)e * D);
+                for (int i = 0; i < C; ++i) {
+                    const long long w = R.off[i] + (i == 0 ? 0 : tu % R.P[i]);
+                    ratios[(size_t)e * C + i] = static_cast<double>(R.count[w]) / static_cast<double>(t.n);
+                    alloc[(size_t)e * C + i] = h_alloc[(size_t)tu * C + i];
+                    const long long p = h_plan[(size_t)tu * C + i];
+                    if (p >= 0) {
+                        auto key = std::make_pair(i, p);
+                        auto it = plan_ids.find(key);
+                        if (it == plan_ids.end()) {
+                            cg_plan cp;
+                            expand_plan(hs[i], p, reps, cp);
+                            it = plan_ids.emplace(key, (int64_t)plans.size()).first;
+                            plans.push_back(cp);
+                        }
+                        eplan[(size_t)e * C + i] = it->second;
+                    }
+                }
+            }
+            std::vector<int64_t> ec(h_ecand.begin(), h_ecand.end());
+            r->eval_candidate = hcopy(ec);
+            r->eval_thresholds = hcopy(thr);
+            r->eval_latency = hcopy(h_eL);
+            r->eval_quality = hcopy(h_eQ);
+            r->eval_ratios = hcopy(ratios);
+            r->eval_allocations = hcopy(alloc);
+            r->eval_plan = hcopy(eplan);
+            r->num_plans = (int64_t)plans.size();
+            r->plans = hcopy(plans);
+            r->num_replicas = (int64_t)reps.size();
+            r->replicas = hcopy(reps);
+            r->num_weights = nw;
+            r->weights = hcopy(weights);
+            std::vector<int32_t> selv(h_sel.begin(), h_sel.end());
+            r->weight_selection = hcopy(selv);
+            r->front_size = h_fsize;
+            std::vector<int64_t> fr(h_front.begin(), h_front.end());
+            r->front = hcopy(fr);
+            r->num_skipped = ncand - nE;
+            std::vector<int64_t> sk(h_skip.begin(), h_skip.end());
+            std::vector<double> skt((size_t)sk.size() * D);
+            for (size_t i = 0; i < sk.size(); ++i) decode_thresholds(sk[i], skt.data() + i * D);
+            r->skipped_candidate = hcopy(sk);
+            r->skipped_thresholds = hcopy(skt);
+            x.st.num_ranks = E->world;
+            x.st.gpu_launches = x.launches;
+            x.st.ms_total = timer.ms();
+            r->stats = x.st;
+        } catch (...) {
+            free_result(r);
+            throw;
+        }
+        *out = r;
+    });
+}
+
+void cg_sweep_result_free(cg_sweep_result* r) { free_result(r); }
+
+cg_status cg_route(cg_engine* E, const cg_trace* tr, const double* thresholds, const int32_t* deployed,
+                   cg_route_result* out, int32_t* accept_stage) {
+    return guarded([&] {
+        if (!E || !tr || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        CG_CUDA(cudaSetDevice(E->device));
+        SweepCtx x(*E);
+        const int C = tr->stages;
+        if (tr->n <= 0) fail(CG_ERR_EMPTY_TRACE, "route_trace: empty trace");
+        int last = -1;
+        for (int i = C - 1; i >= 0; --i)
+            if (deployed[i]) {
+                last = i;
+                break;
+            }
+        if (last < 0) fail(CG_ERR_NO_DEPLOYED_STAGE, "route_trace: no deployed stage");
+        if (C <= 0) fail(CG_ERR_INVALID_INPUT, "route_trace: thresholds length != C-1");
+        if (C > kMaxStages) fail(CG_ERR_UNSUPPORTED, "GPU engine supports up to 5 cascade stages");
+        TraceDev t = trace_to_device(x, *tr);
+        const double rate = overall_rate(t);
+        const int D = C - 1;
+        // Deployment mask folded into one threshold per dimension: undeployed
+        // stages never accept (+inf), the last deployed stage accepts all (-inf).
+        std::vector<std::vector<double>> one(D);
+        std::vector<double> eff(std::max(1, D));
+        for (int d = 0; d < D; ++d) {
+            double h = thresholds[d];
+            if (!deployed[d]) h = dinf();
+            if (d == last) h = -dinf();
+            if (d > last) h = -dinf();
+            eff[d] = h;
+            one[d] = {h};
+        }
+        RoutingOut R = route_all(x, t, one, rate, nullptr);
+        out->stages = C;
+        for (int i = 0; i < C && i < 8; ++i) {
+            const long long w = R.off[i];  // single prefix (all m_d = 0)
+            const bool reached = deployed[i] && i <= last;
+            out->ratios[i] = reached ? static_cast<double>(R.count[w]) / static_cast<double>(t.n) : 0.0;
+            if (reached) {
+                out->stage_workloads[i] = {R.stats[(size_t)w * 5 + 0], R.stats[(size_t)w * 5 + 1],
+                                           R.stats[(size_t)w * 5 + 2], R.stats[(size_t)w * 5 + 3],
+                                           R.stats[(size_t)w * 5 + 4]};
+            } else {
+                out->stage_workloads[i] = {rate * 0.0, 0, 0, 0, 0};
+            }
+        }
+        // quality of the single tuple
+        double qs = 0;
+        x.d2h(&qs, E->d_qsum.p, 8);
+        x.sync();
+        out->quality = qs / static_cast<double>(t.n);
+        if (accept_stage) {
+            double* dh = E->d_misc.as<double>(std::max(1, C));
+            int* ddep = E->d_dep.as<int>(std::max(1, C));
+            int* dout = E->d_acc.as<int>((size_t)t.n);
+            std::vector<double> hh(thresholds, thresholds + D);
+            hh.resize(std::max(1, C), 0.0);
+            std::vector<int> dep(deployed, deployed + C);
+            x.h2d(dh, hh.data(), hh.size() * 8);
+            x.h2d(ddep, dep.data(), dep.size() * 4);
+            k_accept_stage<<<(unsigned)((t.n + 255) / 256), 256, 0, x.s>>>(t.scores, t.n, C, dh, last, ddep, dout);
+            CG_LAUNCH_CHECK();
+            x.d2h(accept_stage, dout, (size_t)t.n * 4);
+            x.sync();
+        }
+    });
+}
+
+cg_status cg_stage_row(cg_engine* E, const cg_model* model, const cg_workload* w, const cg_hardware* hw,
+                       const cg_cost_params* q, int32_t max_budget, cg_row_result** out) {
+    return guarded([&] {
+        if (out) *out = nullptr;
+        if (!E || !model || !w || !hw || !q || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        CG_CUDA(cudaSetDevice(E->device));
+        Timer timer;
+        SweepCtx x(*E);
+        validate_hw(*hw);
+        validate_params(*q);
+        const double ws[5] = {w->arrival_rate, w->mean_input_tokens, w->mean_output_tokens, w->p95_input_tokens,
+                              w->p95_output_tokens};
+        const std::string prob = workload_problems(ws);
+        if (!prob.empty()) fail(CG_ERR_INVALID_INPUT, prob);
+        if (max_budget < 0) fail(CG_ERR_INVALID_INPUT, "row: max_budget must be >= 0");
+        const int N = max_budget;
+        auto* r = static_cast<cg_row_result*>(std::calloc(1, sizeof(cg_row_result)));
+        r->max_budget = N;
+        r->latency = static_cast<double*>(std::malloc(sizeof(double) * (N + 1)));
+        r->plan_index = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (N + 1)));
+        std::vector<cg_plan> plans;
+        std::vector<cg_replica> reps;
+        for (int f = 0; f <= N; ++f) {
+            r->latency[f] = w->arrival_rate == 0.0 ? 0.0 : dinf();
+            r->plan_index[f] = -1;
+        }
+        if (w->arrival_rate != 0.0 && N >= 1) {
+            cg_model m = *model;
+            auto hs = build_spaces(x, &m, 1, *hw, *q, N);
+            std::vector<RowDesc> rows(1);
+            rows[0] = RowDesc{0, 0, row_class(hs[0], N), hs[0].min_gpus > 0 ? N / hs[0].min_gpus : 0,
+                              ws[0], ws[1], ws[2], ws[3], ws[4]};
+            evaluate_rows(x, rows, hs, *hw, *q, N);
+            std::vector<double> lat(N + 1);
+            std::vector<long long> pl(N + 1);
+            x.d2h(lat.data(), E->d_flat.p, (N + 1) * 8);
+            x.d2h(pl.data(), E->d_fplan.p, (N + 1) * 8);
+            x.sync();
+            std::map<long long, int64_t> ids;
+            for (int f = 0; f <= N; ++f) {
+                r->latency[f] = lat[f];
+                if (pl[f] >= 0) {
+                    auto it = ids.find(pl[f]);
+                    if (it == ids.end()) {
+                        cg_plan cp;
+                        expand_plan(hs[0], pl[f], reps, cp);
+                        it = ids.emplace(pl[f], (int64_t)plans.size()).first;
+                        plans.push_back(cp);
+                    }
+                    r->plan_index[f] = it->second;
+                }
+            }
+        }
+        r->num_plans = (int64_t)plans.size();
+        r->plans = hcopy(plans);
+        r->num_replicas = (int64_t)reps.size();
+        r->replicas = hcopy(reps);
+        x.st.gpu_launches = x.launches;
+        x.st.unique_rows = 1;
+        x.st.ms_total = timer.ms();
+        r->stats = x.st;
+        *out = r;
+    });
+}
+
+void cg_row_result_free(cg_row_result* r) {
+    if (!r) return;
+    std::free(r->latency);
+    std::free(r->plan_index);
+    std::free(r->plans);
+    std::free(r->replicas);
+    std::free(r);
+}
+
+cg_status cg_solve_min_max(cg_engine* E, const double* entries, int32_t stages, int32_t gpu_budget,
+                           int32_t total_gpus, int32_t* allocations, double* per_stage_latency,
+                           double* objective_L) {
+    return guarded([&] {
+        if (!E || !entries) fail(CG_ERR_INVALID_INPUT, "null argument");
+        CG_CUDA(cudaSetDevice(E->device));
+        SweepCtx x(*E);
+        // validate_table (innerplan.cpp:58-93)
+        const int n = gpu_budget;
+        if (n < 0) fail(CG_ERR_INVALID_INPUT, "latency table: negative budget");
+        if (stages <= 0) fail(CG_ERR_INVALID_INPUT, "latency table: no stages");
+        for (int i = 0; i < stages; ++i) {
+            bool seen = false;
+            double prev = dinf();
+            for (int f = 0; f <= n; ++f) {
+                const double cell = entries[(size_t)i * (n + 1) + f];
+                if (std::isinf(cell)) {
+                    if (seen && f > 0) fail(CG_ERR_INVALID_INPUT, "latency table: feasibility not upward-closed");
+                    continue;
+                }
+                if (cell < 0.0) fail(CG_ERR_INVALID_INPUT, "latency table: negative latency");
+                if (seen && cell > prev) fail(CG_ERR_INVALID_INPUT, "latency table: row not non-increasing");
+                seen = true;
+                prev = cell;
+            }
+        }
+        if (total_gpus < 0 || total_gpus > gpu_budget)
+            fail(CG_ERR_INVALID_INPUT, "solve_min_max: budget outside table range");
+        if (stages > kMaxStages) fail(CG_ERR_UNSUPPORTED, "GPU engine supports up to 5 cascade stages");
+        const size_t cells = (size_t)stages * (n + 1);
+        double* dlat = E->d_flat.as<double>(cells);
+        long long* dplan = E->d_fplan.as<long long>(cells);
+        x.h2d(dlat, entries, cells * 8);
+        CG_CUDA(cudaMemsetAsync(dplan, 0xff, cells * 8, x.s));
+        std::vector<unsigned long long> cnt(stages, 1);
+        std::vector<int> rowid(stages);
+        for (int i = 0; i < stages; ++i) rowid[i] = i;
+        unsigned long long* dcnt = E->d_wcount.as<unsigned long long>(stages);
+        int* drow = E->d_wlrow.as<int>(stages);
+        x.h2d(dcnt, cnt.data(), stages * 8);
+        x.h2d(drow, rowid.data(), stages * 4);
+        SolveArgs sa{};
+        sa.C = stages;
+        sa.N = n;
+        sa.total_gpus = total_gpus;
+        sa.raw_f0 = 1;
+        sa.ntuples = 1;
+        for (int i = 0; i <= stages; ++i) sa.wl_off[i] = i;
+        for (int i = 0; i < stages; ++i) sa.wl_P[i] = 1;
+        sa.wl_count = dcnt;
+        sa.wl_row = drow;
+        sa.final_lat = dlat;
+        sa.final_plan = dplan;
+        sa.feasible = E->d_tfeas.as<unsigned char>(1);
+        sa.L = E->d_tL.as<double>(1);
+        sa.alloc = E->d_talloc.as<int>(stages);
+        sa.plan = E->d_tplan.as<long long>(stages);
+        launch_solve(sa, x.s, &x.launches);
+        unsigned char feas = 0;
+        double L = 0;
+        std::vector<int> al(stages);
+        x.d2h(&feas, sa.feasible, 1);
+        x.d2h(&L, sa.L, 8);
+        x.d2h(al.data(), sa.alloc, stages * 4);
+        x.sync();
+        if (!feas) fail(CG_ERR_INFEASIBLE_PROBLEM, "no allocation satisfies the GPU budget");
+        for (int i = 0; i < stages; ++i) {
+            if (allocations) allocations[i] = al[i];
+            if (per_stage_latency) per_stage_latency[i] = entries[(size_t)i * (n + 1) + al[i]];
+        }
+        if (objective_L) *objective_L = L;
+    });
+}
+
+}  // extern "C"

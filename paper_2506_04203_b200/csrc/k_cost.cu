@@ -1,0 +1,686 @@
+// K4-K5: the analytical cost model over the allocation x parallelism space.
+//
+// Reference: proj/src/costmodel.cpp
+//   memory_feasible        :79-88     service_time        :176-194
+//   enumerate_multisets    :132-146   plan_set            :205-229
+//   simulate_plan_p95      :248-292   StageEvaluator::row :296-414
+//
+// One "row" = one (stage model, WorkloadStats) pair; its value is
+// latency[f] = min over stable plans using <= f GPUs of the simulated p95
+// sojourn of a 2000-request FCFS join-shortest-queue replay, with the
+// reference's deterministic tie-breaks (parts-lexicographic at equal
+// latency, smaller budget on prefix ties).
+//
+// Design (B200):
+//   * plans are never materialised: a plan index is unranked from the
+//     multiset counting table ways[i][b] and successors come from a
+//     lexicographic odometer -- exactly the reference's recursion order;
+//   * one plan per group of W lanes, one replica per lane (R replicas per
+//     lane beyond 32).  The JSQ choice for a request is a ballot over idle
+//     replicas (lowest index wins, the reference's early break) and, only
+//     when every replica is busy, a butterfly min over (queue length, index);
+//   * per-replica FIFO of waiting finish times in a shared-memory ring with
+//     the in-service finish time in a register; a ring overflow re-runs the
+//     plan in the DEEP instantiation whose rings live in global memory;
+//   * sojourns stream to a per-group scratch column; the exact p95 (the K-th
+//     largest, K = n - (ceil(0.95 n) - 1)) is a group-cooperative 8-bit radix
+//     select, run only for plans that complete;
+//   * exact pruning: once K sojourns of a plan exceed the best latency already
+//     found at a budget <= its GPU count, its p95 is strictly larger, so it
+//     can never appear in the row (neither as best-at-g nor as a prefix
+//     minimum) and the simulation stops.  Row results do not depend on it;
+//   * fp64 uses explicit _rn intrinsics, TU compiled with --fmad=false (H2).
+#include <cuda_runtime.h>
+
+#include "cg_cuda.h"
+#include "cg_internal.h"
+#include "cg_kernels.h"
+#include "plan_dev.cuh"
+
+namespace cg {
+
+namespace {
+
+constexpr double kClampedExpMeanFactor = 0.98168436111126578;  // costmodel.hpp:25
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Row setup
+
+__device__ bool dev_memory_feasible(int tp, int pp, const ModelArgs& m, const HwArgs& hw,
+                                    const ParamArgs& p, double kv_tokens) {
+    const double gpus = (double)(tp * pp);
+    const double weights = __dmul_rn(m.param_count, m.bytes_per_param);
+    if (__ddiv_rn(weights, gpus) > hw.mem_capacity) return false;
+    const double kv_budget =
+        __dmul_rn(p.kv_memory_fraction, __dsub_rn(__dmul_rn(gpus, hw.mem_capacity), weights));
+    return kv_budget >= __dmul_rn(m.kv_bytes_per_token, kv_tokens);
+}
+
+__global__ void k_row_shapes(RowSetupArgs a) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)a.nrows * kMaxShapes) return;
+    const int row = (int)(t / kMaxShapes), s = (int)(t % kMaxShapes);
+    const RowDesc rd = a.rows[row];
+    const PlanSpace& sp = a.spaces[rd.space];
+    const long long o = (long long)row * kMaxShapes + s;
+    if (s >= sp.S) {
+        a.tab.shape_ok[o] = 0;
+        return;
+    }
+    const ModelArgs m = a.models[rd.stage];
+    const int tp = sp.shapes[s].tp, pp = sp.shapes[s].pp;
+    const double kv_tokens = __dadd_rn(rd.p95_in, rd.p95_out);
+    const bool ok = dev_memory_feasible(tp, pp, m, a.hw, a.p, kv_tokens);
+    a.tab.shape_ok[o] = ok ? 1 : 0;
+    if (!ok) {
+        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = 0.0;
+        return;
+    }
+    // service_time (costmodel.cpp:176-194) with the reference's op order
+    const double gpus = (double)(tp * pp);
+    const double bubble = __dadd_rn(1.0, __dmul_rn(a.p.pipeline_bubble_factor, (double)(pp - 1)));
+    const double flops = __dmul_rn(__dmul_rn(2.0, m.param_count), rd.mean_in);
+    const double denom = __dmul_rn(__dmul_rn(gpus, a.hw.flops), a.p.prefill_efficiency);
+    const double comm = __dmul_rn((double)pp, a.p.comm_overhead_per_stage);
+    const double prefill = __dmul_rn(__dadd_rn(__ddiv_rn(flops, denom), comm), bubble);
+    const double weights = __dmul_rn(m.param_count, m.bytes_per_param);
+    const double bw = __dmul_rn(__dmul_rn((double)tp, a.hw.mem_bandwidth), a.p.decode_bw_efficiency);
+    const double decode = __dadd_rn(__ddiv_rn(weights, bw), comm);
+    const double clamped_mean_out = __dmul_rn(rd.mean_out, kClampedExpMeanFactor);
+    a.tab.prefill[o] = prefill;
+    a.tab.decode[o] = decode;
+    a.tab.mean_service[o] = __dadd_rn(prefill, __dmul_rn(clamped_mean_out, decode));
+}
+
+// Common random numbers (costmodel.cpp:331-342).  L[k] = log1p(-u_k) comes
+// from glibc on the host (hazard H3); exponential_mean(m) = (-m) * L.
+__global__ void k_row_crn(RowSetupArgs a, const double* __restrict__ L) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= a.nrows) return;
+    const RowDesc rd = a.rows[row];
+    double* T = a.tab.T + (long long)row * a.n_req;
+    double* O = a.tab.O + (long long)row * a.n_req;
+    const double cap = __dmul_rn(4.0, rd.mean_out);
+    const double neg_mean = -rd.mean_out;
+    double t = 0.0;
+    for (int k = 0; k < a.n_req; ++k) {
+        t = __dadd_rn(t, __ddiv_rn(-L[2 * k], rd.rate));
+        T[k] = t;
+        const double x = __dmul_rn(neg_mean, L[2 * k + 1]);
+        O[k] = (cap < x) ? cap : x;  // std::min(x, cap)
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4
+
+enum : int { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2, ST_FINISH = 3 };
+
+struct GroupShared {
+    unsigned long long plan;  // current plan index
+    unsigned long long hi;    // end of current item (exclusive)
+    int row;
+    int used;   // GPUs of the current count vector
+    int dp;
+    int status;
+    int has_item;
+    int pad;
+    unsigned char counts[kMaxShapes];
+    unsigned hist[256];
+};
+
+template <int W, int R, bool DEEP>
+struct Traits {
+    static constexpr int G = 32 / W;
+    static constexpr int CAP = R == 1 ? 32 : (R == 2 ? 16 : 8);
+    static constexpr size_t ring_bytes_per_warp = DEEP ? 0 : (size_t)32 * R * CAP * sizeof(double);
+    static constexpr size_t bytes_per_warp = ring_bytes_per_warp + G * sizeof(GroupShared);
+};
+
+__device__ __forceinline__ void count_add(unsigned long long* ctr, unsigned long long v) {
+    if (v) atomicAdd(ctr, v);
+}
+
+// Leader lane: advance to the next stable plan (or mark the group done).
+template <bool DEEP>
+__device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
+    while (true) {
+        if (gs.has_item && gs.plan + 1 < gs.hi) {
+            const PlanSpace& sp = a.spaces[a.rows[gs.row].space];
+            int used = gs.used;
+            next_plan(sp, gs.counts, used);
+            gs.used = used;
+            gs.plan += 1;
+        } else {
+            const unsigned long long it = atomicAdd(a.item_counter, 1ull);
+            if (it >= a.nitems) {
+                gs.status = ST_DONE;
+                gs.has_item = 0;
+                return;
+            }
+            int row;
+            unsigned long long lo, hi;
+            if (DEEP) {
+                const SimItem si = a.deep_items[it];
+                row = si.row;
+                lo = si.lo;
+                hi = si.hi;
+            } else {
+                int l = 0, h = a.nrows - 1;  // item_prefix[l] <= it < item_prefix[l+1]
+                while (l < h) {
+                    const int mid = (l + h + 1) >> 1;
+                    if (a.item_prefix[mid] <= it) l = mid;
+                    else h = mid - 1;
+                }
+                row = a.row_ids[l];
+                const unsigned long long j = it - a.item_prefix[l];
+                const unsigned long long P = a.spaces[a.rows[row].space].num_plans;
+                hi = P - j * (unsigned long long)a.item_plans;  // descending items
+                lo = hi > (unsigned long long)a.item_plans ? hi - a.item_plans : 0ull;
+            }
+            gs.row = row;
+            gs.plan = lo;
+            gs.hi = hi;
+            gs.has_item = 1;
+            gs.used = unrank_plan(a.spaces[a.rows[row].space], lo, gs.counts);
+        }
+        // stability filter (costmodel.cpp:366-376), parts order = ascending shape
+        const RowDesc& rd = a.rows[gs.row];
+        const PlanSpace& sp = a.spaces[rd.space];
+        const unsigned char* ok = a.tab.shape_ok + (long long)gs.row * kMaxShapes;
+        const double* ms = a.tab.mean_service + (long long)gs.row * kMaxShapes;
+        bool good = true;
+        double capacity = 0.0;
+        int dp = 0;
+        for (int s = 0; s < sp.S; ++s) {
+            const int c = gs.counts[s];
+            if (!c) continue;
+            if (!ok[s]) {
+                good = false;
+                break;
+            }
+            capacity = __dadd_rn(capacity, __ddiv_rn((double)c, ms[s]));
+            dp += c;
+        }
+        if (!good || rd.rate >= capacity) continue;
+        if (!DEEP) atomicAdd(&a.counters[CTR_STABLE], 1ull);
+        gs.dp = dp;
+        gs.status = ST_RUN;
+        return;
+    }
+}
+
+// Group-cooperative exact K-th largest of n non-negative doubles (8-bit
+// radix select on the IEEE bit patterns, constant bytes skipped).
+template <int W>
+__device__ unsigned long long group_kth_largest(const double* __restrict__ buf, int n, int K, int gl,
+                                                unsigned gm, int gshift, unsigned* hist) {
+    unsigned long long o = 0, an = ~0ull;
+    for (int i = gl; i < n; i += W) {
+        const unsigned long long k = (unsigned long long)__double_as_longlong(buf[i]);
+        o |= k;
+        an &= k;
+    }
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {
+        o |= __shfl_xor_sync(gm, o, off, W);
+        an &= __shfl_xor_sync(gm, an, off, W);
+    }
+    const unsigned long long varying = o ^ an;
+    unsigned long long prefix = 0, pmask = 0;
+    int need = K;
+    for (int byte = 7; byte >= 0; --byte) {
+        const int shift = 8 * byte;
+        const unsigned long long dm = 255ull << shift;
+        if ((varying & dm) == 0) {
+            prefix |= an & dm;
+            pmask |= dm;
+            continue;
+        }
+        for (int b = gl; b < 256; b += W) hist[b] = 0;
+        __syncwarp(gm);
+        for (int i = gl; i < n; i += W) {
+            const unsigned long long k = (unsigned long long)__double_as_longlong(buf[i]);
+            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255ull], 1u);
+        }
+        __syncwarp(gm);
+        constexpr int B = 256 / W;
+        const int top = 255 - gl * B;
+        int seg = 0;
+#pragma unroll
+        for (int j = 0; j < B; ++j) seg += hist[top - j];
+        int incl = seg;
+#pragma unroll
+        for (int off = 1; off < W; off <<= 1) {
+            const int v = __shfl_up_sync(gm, incl, off, W);
+            if (gl >= off) incl += v;
+        }
+        int excl = incl - seg;
+        const bool mine = excl < need && need <= incl;
+        int digit = 0, before = 0;
+        if (mine) {
+            for (int j = 0; j < B; ++j) {
+                const int c = hist[top - j];
+                if (excl + c >= need) {
+                    digit = top - j;
+                    before = excl;
+                    break;
+                }
+                excl += c;
+            }
+        }
+        const unsigned ob = __ballot_sync(gm, mine);
+        const int owner = (__ffs(ob) - 1) - gshift;
+        digit = __shfl_sync(gm, digit, owner, W);
+        before = __shfl_sync(gm, before, owner, W);
+        prefix |= (unsigned long long)digit << shift;
+        pmask |= dm;
+        need -= before;
+        __syncwarp(gm);
+    }
+    return prefix;
+}
+
+template <int W, int R, bool DEEP>
+__global__ void __launch_bounds__(128) k_sim(SimArgs a) {
+    using TR = Traits<W, R, DEEP>;
+    constexpr int G = TR::G;
+    constexpr int CAP = TR::CAP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gid = lane / W;
+    const int gl = lane % W;
+    const int gshift = gid * W;
+    const unsigned wmask = (W == 32) ? FULL : ((1u << W) - 1u);
+    const unsigned gm = wmask << gshift;
+
+    unsigned char* wbase = smem + (size_t)warp * TR::bytes_per_warp;
+    double* ring = reinterpret_cast<double*>(wbase);
+    GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes_per_warp);
+    GroupShared& gs = gsa[gid];
+
+    const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+    const long long slot = gwarp * G + gid;
+    double* scratch = a.scratch + slot * (long long)a.n_req;
+    double* gring = DEEP ? a.ring_global + gwarp * (long long)32 * R * a.ring_cap : nullptr;
+    const int ring_mask = DEEP ? a.ring_cap - 1 : CAP - 1;
+    const int ring_cap = DEEP ? a.ring_cap : CAP;
+
+    if (gl == 0) {
+        gs.status = ST_NEED;
+        gs.has_item = 0;
+    }
+    __syncwarp();
+
+    int status = ST_NEED;
+    int row = 0, dp = 0, gpus = 0, k = 0, ab = 0;
+    unsigned long long plan = 0;
+    bool ovf = false;
+    double U = __longlong_as_double((long long)kInfBits);
+    const double* Trow = nullptr;
+    const double* Orow = nullptr;
+    double nd[R], avail[R], pre[R], dec[R];
+    int cnt[R], head[R], tail[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        nd[r] = avail[r] = pre[r] = dec[r] = 0.0;
+        cnt[r] = head[r] = tail[r] = 0;
+    }
+    unsigned long long steps = 0, full = 0, pruned = 0;
+    const double INF = __longlong_as_double((long long)kInfBits);
+
+    for (unsigned it = 0;; ++it) {
+        // ---- phase A: groups without a plan acquire one
+        const bool need = status == ST_NEED;
+        if (__any_sync(FULL, need)) {
+            if (need && gl == 0) acquire_plan<DEEP>(a, gs);
+            __syncwarp();
+            if (need) {
+                status = gs.status;
+                if (status == ST_RUN) {
+                    row = gs.row;
+                    dp = gs.dp;
+                    gpus = gs.used;
+                    plan = gs.plan;
+                    const PlanSpace& sp = a.spaces[a.rows[row].space];
+                    Trow = a.tab.T + (long long)row * a.n_req;
+                    Orow = a.tab.O + (long long)row * a.n_req;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int j = r * W + gl;
+                        nd[r] = INF;
+                        avail[r] = 0.0;
+                        cnt[r] = head[r] = tail[r] = 0;
+                        if (j < dp) {
+                            int cum = 0, s = 0;
+                            for (; s < sp.S; ++s) {
+                                cum += gs.counts[s];
+                                if (j < cum) break;
+                            }
+                            pre[r] = a.tab.prefill[(long long)row * kMaxShapes + s];
+                            dec[r] = a.tab.decode[(long long)row * kMaxShapes + s];
+                        }
+                    }
+                    k = 0;
+                    ab = 0;
+                    ovf = false;
+                    U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus])
+                                : INF;
+                }
+            }
+            __syncwarp();
+        }
+        if (__all_sync(FULL, status == ST_DONE)) break;
+
+        // ---- phase B: one JSQ dispatch step per running group
+        const bool run = status == ST_RUN;
+        double t = 0.0, o = 0.0;
+        if (run) {
+            t = __ldg(&Trow[k]);
+            o = __ldg(&Orow[k]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            while (nd[r] <= t && run) {  // departures up to t (fin <= t has left)
+                --cnt[r];
+                if (cnt[r] > 0) {
+                    const int slotr = head[r] & ring_mask;
+                    nd[r] = DEEP ? gring[((long long)r * ring_cap + slotr) * 32 + lane]
+                                 : ring[(r * CAP + slotr) * 32 + lane];
+                    ++head[r];
+                } else {
+                    nd[r] = INF;
+                }
+            }
+        }
+        int win = -1;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const bool idle = run && cnt[r] == 0 && (r * W + gl) < dp;
+            const unsigned gb = (__ballot_sync(FULL, idle) >> gshift) & wmask;
+            if (win < 0 && gb) win = r * W + (__ffs(gb) - 1);
+        }
+        const bool all_busy = run && win < 0;
+        if (__any_sync(FULL, all_busy)) {
+            unsigned key = 0xffffffffu;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int j = r * W + gl;
+                if (j < dp) {
+                    const unsigned kk = ((unsigned)cnt[r] << 9) | (unsigned)j;
+                    key = kk < key ? kk : key;
+                }
+            }
+#pragma unroll
+            for (int off = W / 2; off > 0; off >>= 1) {
+                const unsigned v = __shfl_xor_sync(FULL, key, off);
+                key = v < key ? v : key;
+            }
+            if (all_busy) win = (int)(key & 511u);
+        }
+        if (run) {
+            if (gl == (win & (W - 1))) {
+                const int wr = win / W;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r == wr) {
+                        const double start = (t < avail[r]) ? avail[r] : t;  // std::max(t, avail)
+                        const double fin = __dadd_rn(__dadd_rn(start, pre[r]), __dmul_rn(o, dec[r]));
+                        const double soj = __dsub_rn(fin, t);
+                        if (cnt[r] == 0) {
+                            nd[r] = fin;
+                        } else {
+                            const int slotr = tail[r] & ring_mask;
+                            if (DEEP) gring[((long long)r * ring_cap + slotr) * 32 + lane] = fin;
+                            else ring[(r * CAP + slotr) * 32 + lane] = fin;
+                            ++tail[r];
+                            if (tail[r] - head[r] > ring_cap) ovf = true;
+                        }
+                        ++cnt[r];
+                        avail[r] = fin;
+                        scratch[k] = soj;
+                        ab += (soj > U) ? 1 : 0;
+                    }
+                }
+            }
+            ++k;
+            if (k == a.n_req) status = ST_FINISH;
+        }
+
+        // ---- phase C: periodic exact-bound pruning and overflow checks
+        if ((it & 31u) == 31u) {
+            int tot = ab;
+            int ov = ovf ? 1 : 0;
+#pragma unroll
+            for (int off = W / 2; off > 0; off >>= 1) {
+                tot += __shfl_xor_sync(FULL, tot, off);
+                ov |= __shfl_xor_sync(FULL, ov, off);
+            }
+            if (status == ST_RUN) {
+                if (ov) {
+                    if (gl == 0) {
+                        const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
+                        if (idx < a.ovf_cap) a.ovf[idx] = SimItem{row, 0, plan, plan + 1};
+                    }
+                    steps += k;
+                    status = ST_NEED;
+                } else if (a.prune && tot >= a.K) {
+                    pruned += 1;
+                    steps += k;
+                    status = ST_NEED;
+                } else if (a.prune) {
+                    U = __longlong_as_double(
+                        (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
+                }
+            }
+            if (status == ST_NEED && gl == 0) gs.status = ST_NEED;
+        }
+
+        // ---- phase D: completed plans -> exact p95 and row bookkeeping
+        if (__any_sync(FULL, status == ST_FINISH)) {
+            if (status == ST_FINISH) {
+                int tot = ab;
+                int ov = ovf ? 1 : 0;
+#pragma unroll
+                for (int off = W / 2; off > 0; off >>= 1) {
+                    tot += __shfl_xor_sync(gm, tot, off, W);
+                    ov |= __shfl_xor_sync(gm, ov, off, W);
+                }
+                steps += k;
+                if (ov) {
+                    if (gl == 0) {
+                        const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
+                        if (idx < a.ovf_cap) a.ovf[idx] = SimItem{row, 0, plan, plan + 1};
+                    }
+                } else if (a.prune && tot >= a.K) {
+                    pruned += 1;
+                } else {
+                    __syncwarp(gm);
+                    const unsigned long long xb =
+                        group_kth_largest<W>(scratch, a.n_req, a.K, gl, gm, gshift, gs.hist);
+                    full += 1;
+                    if (gl == 0) {
+                        const long long base = (long long)row * (a.N + 1);
+                        const unsigned long long old = atomicMin(&a.lat_min[base + gpus], xb);
+                        if (xb <= old) {
+                            const unsigned long long idx = atomicAdd(a.tie_count, 1ull);
+                            if (idx < a.tie_cap) a.ties[idx] = TieEntry{row, gpus, xb, plan};
+                        }
+                        for (int g2 = gpus; g2 <= a.N; ++g2) {
+                            unsigned long long* ub = &a.ub[base + g2];
+                            if (*(volatile unsigned long long*)ub <= xb) break;
+                            atomicMin(ub, xb);
+                        }
+                    }
+                }
+                status = ST_NEED;
+                if (gl == 0) gs.status = ST_NEED;
+            }
+            __syncwarp();
+        }
+    }
+    // per-lane counters -> global (leaders only to avoid double counting)
+    if (gl == 0) {
+        count_add(&a.counters[CTR_STEPS], steps);
+        count_add(&a.counters[CTR_FULL], full);
+        count_add(&a.counters[CTR_PRUNED], pruned);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: tie resolution and the prefix minimum over budgets
+
+__global__ void k_resolve_ties(ResolveArgs a) {
+    const unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (e >= a.nties) return;
+    const TieEntry te = a.ties[e];
+    const long long cell = (long long)te.row * (a.N + 1) + te.g;
+    if (te.lat_bits != a.lat_min[cell]) return;
+    const PlanSpace& sp = a.spaces[a.rows[te.row].space];
+    unsigned char A[kMaxShapes], B[kMaxShapes];
+    unrank_plan(sp, te.plan, A);
+    unsigned long long cur = *(volatile unsigned long long*)&a.best_plan[cell];
+    while (true) {
+        if (cur != kEmpty) {
+            if (cur == te.plan) return;
+            unrank_plan(sp, cur, B);
+            if (!parts_less(A, B, sp.S)) return;
+        }
+        const unsigned long long prev = atomicCAS(&a.best_plan[cell], cur, te.plan);
+        if (prev == cur) return;
+        cur = prev;
+    }
+}
+
+// StageEvaluator::row prefix minimum (costmodel.cpp:398-412): strict '<' so
+// ties keep the smaller budget; f = 0 is never assigned for live rows.
+__global__ void k_row_prefix(ResolveArgs a) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= a.nrows) return;
+    const long long base = (long long)row * (a.N + 1);
+    double running = __longlong_as_double((long long)kInfBits);
+    long long running_plan = -1;
+    a.final_lat[base] = running;
+    a.final_plan[base] = -1;
+    for (int f = 1; f <= a.N; ++f) {
+        const unsigned long long p = a.best_plan[base + f];
+        if (p != kEmpty) {
+            const double l = __longlong_as_double((long long)a.lat_min[base + f]);
+            if (l < running) {
+                running = l;
+                running_plan = (long long)p;
+            }
+        }
+        a.final_lat[base + f] = running;
+        a.final_plan[base + f] = running_plan;
+    }
+}
+
+template <int W, int R, bool DEEP>
+void launch_sim_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches, int* grid_out) {
+    using TR = Traits<W, R, DEEP>;
+    const size_t smem = TR::bytes_per_warp * 4;
+    auto kern = k_sim<W, R, DEEP>;
+    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    if (per_sm < 1) per_sm = 1;
+    int grid = sm_count * per_sm;
+    if (DEEP && grid > sm_count) grid = sm_count;
+    if (grid_out) *grid_out = grid;
+    if (a.nitems == 0) return;
+    kern<<<grid, 128, smem, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
+}
+
+}  // namespace
+
+SimGeometry sim_geometry(int cls, bool deep, int sm_count) {
+    // must mirror launch_sim's grid choice: slots = grid * 4 warps * G
+    SimGeometry g{};
+    int W = 32, R = 1;
+    class_shape(cls, &W, &R);
+    if (deep) W = 32;
+    g.W = W;
+    g.R = R;
+    g.G = 32 / W;
+    int grid = 0;
+    SimArgs dummy{};
+    dummy.nitems = 0;
+    launch_sim(dummy, cls, deep, sm_count, nullptr, nullptr, &grid);
+    g.grid = grid;
+    g.slots = (long long)grid * 4 * g.G;
+    g.warps = (long long)grid * 4;
+    return g;
+}
+
+void class_shape(int cls, int* W, int* R) {
+    static const int Ws[7] = {4, 8, 16, 32, 32, 32, 32};
+    static const int Rs[7] = {1, 1, 1, 1, 2, 4, 8};
+    *W = Ws[cls];
+    *R = Rs[cls];
+}
+
+int class_for_dp(int dpmax) {
+    if (dpmax <= 4) return 0;
+    if (dpmax <= 8) return 1;
+    if (dpmax <= 16) return 2;
+    if (dpmax <= 32) return 3;
+    if (dpmax <= 64) return 4;
+    if (dpmax <= 128) return 5;
+    if (dpmax <= 256) return 6;
+    return -1;
+}
+
+void launch_sim(const SimArgs& a, int cls, bool deep, int sm_count, cudaStream_t s, int* launches,
+                int* grid_out) {
+    if (deep) {
+        switch (cls) {
+            case 0: case 1: case 2: case 3: launch_sim_t<32, 1, true>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, true>(a, sm_count, s, launches, grid_out); return;
+            case 5: launch_sim_t<32, 4, true>(a, sm_count, s, launches, grid_out); return;
+            case 6: launch_sim_t<32, 8, true>(a, sm_count, s, launches, grid_out); return;
+        }
+    } else {
+        switch (cls) {
+            case 0: launch_sim_t<4, 1, false>(a, sm_count, s, launches, grid_out); return;
+            case 1: launch_sim_t<8, 1, false>(a, sm_count, s, launches, grid_out); return;
+            case 2: launch_sim_t<16, 1, false>(a, sm_count, s, launches, grid_out); return;
+            case 3: launch_sim_t<32, 1, false>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, false>(a, sm_count, s, launches, grid_out); return;
+            case 5: launch_sim_t<32, 4, false>(a, sm_count, s, launches, grid_out); return;
+            case 6: launch_sim_t<32, 8, false>(a, sm_count, s, launches, grid_out); return;
+        }
+    }
+    throw EngineError(101, "unsupported JSQ kernel class");
+}
+
+void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches) {
+    if (a.nrows == 0) return;
+    const long long work = (long long)a.nrows * kMaxShapes;
+    k_row_shapes<<<(unsigned)((work + 127) / 128), 128, 0, s>>>(a);
+    CG_LAUNCH_CHECK();
+    k_row_crn<<<(unsigned)((a.nrows + 63) / 64), 64, 0, s>>>(a, L);
+    CG_LAUNCH_CHECK();
+    if (launches) *launches += 2;
+}
+
+void launch_resolve(const ResolveArgs& a, cudaStream_t s, int* launches) {
+    if (a.nties > 0) {
+        k_resolve_ties<<<(unsigned)((a.nties + 127) / 128), 128, 0, s>>>(a);
+        CG_LAUNCH_CHECK();
+        if (launches) ++*launches;
+    }
+    if (a.nrows > 0) {
+        k_row_prefix<<<(unsigned)((a.nrows + 127) / 128), 128, 0, s>>>(a);
+        CG_LAUNCH_CHECK();
+        if (launches) ++*launches;
+    }
+}
+
+}  // namespace cg

@@ -1,0 +1,71 @@
+// Device-side plan-space helpers shared by the cost-model kernels and the
+// cross-rank merge: unranking, lexicographic successor, parts comparator.
+//
+// Plan order = the reference's enumerate_multisets recursion
+// (proj/src/costmodel.cpp:132-146): count vectors (c_0..c_{S-1}) over the
+// canonical shape list in lexicographic order, the empty multiset skipped.
+#pragma once
+
+#include "cg_internal.h"
+
+namespace cg {
+
+__device__ __forceinline__ unsigned long long ways_at(const PlanSpace& sp, int i, int b) {
+    return sp.ways[(long long)i * (sp.N + 1) + b];
+}
+
+// plan index p (0-based) -> counts; returns the GPUs used
+__device__ inline int unrank_plan(const PlanSpace& sp, unsigned long long p, unsigned char* c) {
+    unsigned long long q = p + 1;  // lexicographic rank including the empty multiset
+    int b = sp.N;
+    int used = 0;
+    for (int i = 0; i < sp.S; ++i) {
+        const int size = sp.shapes[i].gpus;
+        int k = 0;
+        while (true) {
+            const unsigned long long w = ways_at(sp, i + 1, b - k * size);
+            if (q < w) break;
+            q -= w;
+            ++k;
+        }
+        c[i] = (unsigned char)k;
+        b -= k * size;
+        used += k * size;
+    }
+    return used;
+}
+
+// successor in the recursion order (last shape fastest); false at the end
+__device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& used) {
+    for (int i = sp.S - 1; i >= 0; --i) {
+        const int size = sp.shapes[i].gpus;
+        if (used + size <= sp.N) {
+            c[i] = (unsigned char)(c[i] + 1);
+            used += size;
+            return true;
+        }
+        used -= c[i] * size;
+        c[i] = 0;
+    }
+    return false;
+}
+
+// '<' of CompactPlan::parts (vector<pair<shape, count>>, costmodel.cpp:351)
+// evaluated on dense count vectors.
+__device__ inline bool parts_less(const unsigned char* A, const unsigned char* B, int S) {
+    for (int s = 0; s < S; ++s) {
+        if (A[s] == B[s]) continue;
+        if (A[s] > 0 && B[s] > 0) return A[s] < B[s];
+        if (A[s] == 0) {  // A's next pair has a larger shape index, or A ended
+            for (int t = s + 1; t < S; ++t)
+                if (A[t]) return false;
+            return true;
+        }
+        for (int t = s + 1; t < S; ++t)
+            if (B[t]) return true;
+        return false;
+    }
+    return false;
+}
+
+}  // namespace cg
