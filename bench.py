@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark: candidate plans evaluated per second by one full plan search
+(cascade::outerplan::sweep) on the B200 engine, vs the reference CPU planner.
+
+A step = one complete sweep of the workload (routing of every threshold
+candidate, every latency row over the allocation x TP/PP/DP space, the inner
+min-max solve, Tchebycheff + Pareto).  The metric's numerator is the number of
+(workload row, parallelism plan) pairs the sweep must decide -- the
+reference's own count (sum over its row cache of |plan set|), identical for
+both arms -- and the denominator the sweep time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+N>1 runs under torchrun: every rank routes redundantly, the cost-model work is
+sharded over ranks and merged with one NCCL all-gather (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "candidate plans evaluated/sec (plan-search sweep)"
+UNIT = "plans/s"
+WORKLOAD_DESC = {
+    "C1": "C1: 2-model Llama-3 8B->70B, 10k-request trace, 16-GPU pool, 32-point grid",
+    "C2": "C2: 3-model R1-Distill 8B->32B->671B, 100k-request trace, 32-GPU pool, 64x64 grid",
+    "C3": "C3: 3-model Llama 8B->70B->405B, 1M-request heterogeneous bursty trace, 64-GPU pool, decile grid",
+    "C4": "C4: C2 cascade, 100k requests, 256x256 grid, 32 Tchebycheff weights",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def build_workload(name: str):
+    from paper_2506_04203_b200 import engine as eng
+    from paper_2506_04203_b200 import workloads as W
+    parts = [eng.generate_trace(s, seed) for s, seed in W.trace_specs(name)]
+    trace = eng.concat_traces(parts) if len(parts) > 1 else parts[0]
+    cfg, N = W.planner_config(name, trace["scores"])
+    return trace, cfg, N
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        loaded = [v for v in sm if v > 500] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_sample(trace, cfg, N, grid_points=4):
+    """The reference CPU planner (oracle/_ref, unmodified sources) timed on a
+    bounded sample of the same workload: same trace/hardware/models, a
+    grid_points^(C-1) threshold grid.  Returns (plans/s, details)."""
+    from oracle import refpy
+    from paper_2506_04203_b200 import workloads as W
+    sample_cfg = json.loads(json.dumps(cfg))
+    sample_cfg["sweep"]["threshold_grid"] = W.explicit_grid(trace["scores"], grid_points)
+    counts = refpy.plan_count(trace, sample_cfg, N)
+    t0 = time.perf_counter()
+    res = refpy.sweep(trace, sample_cfg, N)
+    wall = time.perf_counter() - t0
+    el = float(res["elapsed_s"])
+    cores = refpy.max_threads()
+    return counts["plans"] / el, {
+        "elapsed_s": el, "wall_s": wall, "plans": counts["plans"], "unique_rows": counts["unique_rows"],
+        "candidates": counts["candidates"], "cores": cores,
+        "sample": f"same trace/models/hardware, {grid_points}^(C-1) grid ({counts['candidates']} candidates, "
+                  f"{counts['unique_rows']} rows, {counts['plans']} plans), CASCADE_PLANNER_THREADS={cores}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    os.environ.setdefault("CASCADE_PLANNER_THREADS", str(os.cpu_count() or 1))
+    from oracle import refpy
+    if not refpy.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcascade_ref.so not built"}))
+        return 0
+    trace, cfg, N = build_workload(args.config)
+    for _ in range(args.warmup):
+        cpu_reference_sample(trace, cfg, N, args.ref_grid)
+    vals, dets = [], []
+    for _ in range(args.steps):
+        v, d = cpu_reference_sample(trace, cfg, N, args.ref_grid)
+        vals.append(v)
+        dets.append(d)
+    value = float(np.mean(vals))
+    ms = float(np.mean([d["elapsed_s"] for d in dets]) * 1000.0)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "sample": dets[0]["sample"]},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": dets[0]["cores"], "kind": "reference",
+                            "sample": dets[0]["sample"]},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+class _DevPtr:
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_04203_b200 import engine as eng
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    trace, cfg, N = build_workload(args.config)
+    E = eng.Engine(local)
+    if world > 1:
+        def allgather(send, recv, nbytes):
+            s = torch.as_tensor(_DevPtr(send, nbytes), device="cuda")
+            r = torch.as_tensor(_DevPtr(recv, nbytes * world), device="cuda")
+            dist.all_gather_into_tensor(r, s)
+            torch.cuda.synchronize()
+        E.set_collective(rank, world, allgather)
+    stream = torch.cuda.ExternalStream(E.stream_handle())
+
+    # HBM-resident trace (value) and pinned host trace (e2e)
+    dev = {k: torch.from_numpy(np.ascontiguousarray(trace[k], dtype=np.float64)).cuda()
+           for k in ("arrival_s", "input_tokens", "output_tokens", "scores")}
+    pin = {k: torch.from_numpy(np.ascontiguousarray(trace[k], dtype=np.float64)).pin_memory()
+           for k in ("arrival_s", "input_tokens", "output_tokens", "scores")}
+    n = int(trace["arrival_s"].shape[0])
+    C = int(trace["scores"].shape[0])
+    tr_dev = eng.TraceBuffers(dev["arrival_s"].data_ptr(), dev["input_tokens"].data_ptr(),
+                              dev["output_tokens"].data_ptr(), dev["scores"].data_ptr(), on_device=True,
+                              keep={"n": n, "stages": C, "t": dev})
+    tr_host = eng.TraceBuffers(pin["arrival_s"].numpy(), pin["input_tokens"].numpy(),
+                               pin["output_tokens"].numpy(), pin["scores"].numpy())
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def one(tr):
+        E.sweep(tr, cfg["models"], cfg["hardware"], cfg["cost_model"], N, cfg["sweep"], raw=True)
+        return dict(E.last_stats)
+
+    def timed(tr, steps):
+        times, stats = [], []
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # L2 flush between timed iterations (outside the events)
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            st = one(tr)
+            s1.record(stream)
+            s1.synchronize()
+            times.append(s0.elapsed_time(s1))
+            stats.append(st)
+        return times, stats
+
+    for _ in range(args.warmup):
+        one(tr_dev)
+        one(tr_host)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_dev, st_dev = timed(tr_dev, args.steps)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_e2e, st_e2e = timed(tr_host, args.steps)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_dev = float(np.sum(t_dev))
+    ms_e2e = float(np.sum(t_e2e))
+    if world > 1:
+        tt = torch.tensor([ms_dev, ms_e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_dev, ms_e2e = float(tt[0]), float(tt[1])
+    plans = st_dev[-1]["plans_enumerated"]
+    value = plans * args.steps / (ms_dev / 1000.0)
+    e2e = plans * args.steps / (ms_e2e / 1000.0)
+
+    if rank == 0:
+        peak, peak_kind = load_peaks()
+        k1_ms = float(np.mean([s["ms_k1"] for s in st_dev]))
+        k1_bytes = st_dev[-1]["k1_bytes"]
+        k1_gbs = k1_bytes / (k1_ms / 1000.0) / 1e9 if k1_ms > 0 else 0.0
+        k4_ms = float(np.mean([s["ms_k4"] for s in st_dev]))
+        steps_k4 = st_dev[-1]["request_steps"]
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "total_gpus_planned": N,
+                       "requests": n, "stages": C, "candidates": st_dev[-1]["candidates"],
+                       "unique_rows": st_dev[-1]["unique_rows"], "plans_per_sweep": plans,
+                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
+                       "parallelism": f"rows sharded over {world} GPU(s), 1 all-gather"},
+            "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
+                    "h2d_bytes_per_step": st_e2e[-1]["h2d_bytes"], "d2h_bytes_per_step": st_e2e[-1]["d2h_bytes"]},
+            "gpu_launches": int(sum(s["gpu_launches"] for s in st_dev) + sum(s["gpu_launches"] for s in st_e2e)),
+            "roofline": {"bound": "hbm", "kernel": "k_route_aggregate (K1 routing/aggregation pass)",
+                         "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": k1_gbs / peak if peak else None, "traffic": None,
+                         "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "ms_per_launch": k1_ms},
+            "roofline_k4": {"bound": "issue", "kernel": "k_sim (K4 JSQ simulation)", "ms_per_sweep": k4_ms,
+                            "request_steps_per_s": steps_k4 / (k4_ms / 1000.0) if k4_ms > 0 else None,
+                            "plans_simulated_full": st_dev[-1]["plans_simulated_full"],
+                            "plans_pruned": st_dev[-1]["plans_pruned"]},
+            "phases_ms": {k: float(np.mean([s[k] for s in st_dev])) for k in
+                          ("ms_route", "ms_quality", "ms_rows", "ms_solve", "ms_total")},
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            os.environ.setdefault("CASCADE_PLANNER_THREADS", str(os.cpu_count() or 1))
+            try:
+                v, d = cpu_reference_sample(trace, cfg, N, args.ref_grid)
+                out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": d["cores"], "kind": "reference",
+                                       "sample": d["sample"], "elapsed_s": d["elapsed_s"]}
+            except Exception as ex:  # reported, never silently replaced
+                out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                                       "sample": f"unavailable: {ex}"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--ref-grid", type=int, default=4, help="grid points per dim of the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -204,6 +204,9 @@ void cg_engine_destroy(cg_engine* engine);
 /* Shard the cost-model work over `world` ranks (this engine is `rank`). */
 cg_status cg_engine_set_collective(cg_engine* engine, int32_t rank, int32_t world,
                                    cg_allgather_fn allgather, void* user);
+/* The engine's CUDA stream (cudaStream_t): every kernel and copy of a call runs
+ * on it, so callers can bracket calls with their own CUDA events. */
+void* cg_engine_stream(cg_engine* engine);
 /* Debug/parity knob: 0 disables the exact p95-bound pruning in K4. */
 cg_status cg_engine_set_option(cg_engine* engine, const char* key, int64_t value);
 

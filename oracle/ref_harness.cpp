@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -287,6 +288,68 @@ char* ref_pareto(const double* latency, const double* quality, std::int64_t n) {
         for (const auto& p : front.points)
             idx.push_back(static_cast<std::int64_t>(p.plan_ref.predicted_max_p95_s));
         return ok(idx, 0.0);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// Counts what one sweep() must decide, with the reference's own APIs: the
+/// unique (stage, WorkloadStats) rows of its row cache (outerplan.cpp:191-203,
+/// live stages only) and the sum of their plan-set sizes (enumerate_plans).
+char* ref_plan_count(const double* arrival, const double* in_tok, const double* out_tok,
+                     const double* scores, std::int64_t n, int c, const char* config_json,
+                     int total_gpus) {
+    try {
+        auto cfg = json::parse(config_json).get<cli::PlannerConfig>();
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        auto grid = cfg.sweep.threshold_grid.empty()
+                        ? outerplan::default_threshold_grid(trace, static_cast<std::size_t>(c))
+                        : cfg.sweep.threshold_grid;
+        std::vector<bool> deployed(c, true);
+        std::map<std::string, int> rows;
+        std::vector<std::size_t> cursor(grid.size(), 0);
+        long long candidates = 0;
+        bool done = false;
+        while (!done) {
+            RoutingThresholds h;
+            for (std::size_t d = 0; d < grid.size(); ++d) h.thresholds.push_back(grid[d][cursor[d]]);
+            auto out = routing::route_trace(trace, h, deployed);
+            ++candidates;
+            for (int i = 0; i < c; ++i) {
+                if (!(out.ratios[i] > 0.0)) continue;
+                const auto& w = out.stage_workloads[i];
+                double f[5] = {w.arrival_rate, w.mean_input_tokens, w.mean_output_tokens,
+                               w.p95_input_tokens, w.p95_output_tokens};
+                std::string key(sizeof(int) + sizeof(f), '\0');
+                std::memcpy(key.data(), &i, sizeof(int));
+                std::memcpy(key.data() + sizeof(int), f, sizeof(f));
+                rows.emplace(key, i);
+            }
+            done = true;
+            for (std::size_t d = grid.size(); d-- > 0;) {
+                if (++cursor[d] < grid[d].size()) { done = false; break; }
+                cursor[d] = 0;
+            }
+            if (grid.empty()) break;
+        }
+        std::vector<long long> per_stage(c, -1);
+        long long plans = 0;
+        for (const auto& kv : rows) {
+            int i = kv.second;
+            if (per_stage[i] < 0)
+                per_stage[i] = total_gpus >= 1
+                    ? static_cast<long long>(costmodel::enumerate_plans(total_gpus, cfg.models[i],
+                                                                        cfg.hardware, cfg.cost_model).size())
+                    : 0;
+            plans += per_stage[i];
+        }
+        json j;
+        j["unique_rows"] = rows.size();
+        j["plans"] = plans;
+        j["candidates"] = candidates;
+        return ok(j, 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
     } catch (const std::exception& e) {
         return fail_std(e);
     }

@@ -45,6 +45,7 @@ def lib():
             "ref_generate_trace": [ctypes.c_char_p, ctypes.c_uint64, _D, _D, _D, _D, ctypes.c_int64],
             "ref_weight_ladder": [ctypes.c_double, ctypes.c_double, ctypes.c_int],
             "ref_pareto": [_D, _D, ctypes.c_int64],
+            "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
         }.items():
             f = getattr(L, name)
             f.argtypes = args
@@ -121,6 +122,12 @@ def plan_outputs(trace: dict, config: dict, total_gpus: int, requirement: dict) 
     return _unwrap(_call(lib().ref_plan_outputs, *map(_ptr, keep), n, c,
                          json.dumps(config).encode(), total_gpus,
                          json.dumps(requirement).encode()))["result"]
+
+
+def plan_count(trace: dict, config: dict, total_gpus: int) -> dict:
+    keep, n, c = _trace_args(trace)
+    return _unwrap(_call(lib().ref_plan_count, *map(_ptr, keep), n, c, json.dumps(config).encode(),
+                         total_gpus))["result"]
 
 
 def route(trace: dict, thresholds, deployed) -> dict:

@@ -305,10 +305,19 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     for (auto& kv : by_cls) {
         const int cls = kv.first;
         const auto& rl = kv.second;
+        // item size: large enough to amortise unranking, small enough that every
+        // group slot of the persistent grid gets >= ~16 items
+        unsigned long long class_plans = 0;
+        for (int r : rl) class_plans += hs[rows[r].space].num_plans;
+        const SimGeometry geo = sim_geometry(cls, false, E.sm_count);
+        const unsigned long long per =
+            std::max<unsigned long long>(1ull, class_plans / ((unsigned long long)geo.slots * 16ull));
+        const int item_plans = (int)std::min<unsigned long long>((unsigned long long)E.item_plans,
+                                                                 std::max<unsigned long long>(4ull, per));
         std::vector<unsigned long long> prefix(rl.size() + 1, 0);
         for (size_t i = 0; i < rl.size(); ++i) {
             const unsigned long long P = hs[rows[rl[i]].space].num_plans;
-            prefix[i + 1] = prefix[i] + (P + E.item_plans - 1) / E.item_plans;
+            prefix[i + 1] = prefix[i] + (P + item_plans - 1) / item_plans;
         }
         const unsigned long long total_items = prefix.back();
         const unsigned long long lo = total_items * (unsigned long long)E.rank / (unsigned long long)E.world;
@@ -326,7 +335,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         a.n_req = n_req;
         a.K = K;
         a.prune = E.prune;
-        a.item_plans = E.item_plans;
+        a.item_plans = item_plans;
         a.nrows = (int)rl.size();
         a.row_ids = rowids;
         a.item_prefix = ipre;
@@ -746,6 +755,8 @@ cg_status cg_engine_create(int32_t device, cg_engine** out) {
         *out = e;
     });
 }
+
+void* cg_engine_stream(cg_engine* e) { return e ? static_cast<void*>(e->s) : nullptr; }
 
 void cg_engine_destroy(cg_engine* e) {
     if (!e) return;

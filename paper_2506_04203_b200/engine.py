@@ -137,7 +137,7 @@ class RowResultC(ctypes.Structure):
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                 ctypes.c_void_p)
 
-EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_set_collective", "cg_engine_set_option",
+EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_engine_set_collective", "cg_engine_set_option",
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
             "cg_solve_min_max", "cg_generate_trace", "cg_version"]
 
@@ -182,6 +182,8 @@ def library():
                                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]
         L.cg_generate_trace.restype = Status
         L.cg_version.restype = ctypes.c_char_p
+        L.cg_engine_stream.argtypes = [ctypes.c_void_p]
+        L.cg_engine_stream.restype = ctypes.c_void_p
         _lib = L
     return _lib
 
@@ -346,6 +348,10 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of the engine (all work of a call runs on it)."""
+        return int(self._lib.cg_engine_stream(self._h) or 0)
 
     def set_option(self, key: str, value: int):
         _check(self._lib.cg_engine_set_option(self._h, key.encode(), int(value)))

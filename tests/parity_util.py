@@ -79,3 +79,10 @@ def parity_cases():
     cfg["hardware"]["gpu_count"] = 16
     cases.append(("c2_small_n16", t, cfg, 16))
     return cases
+
+
+def golden_trace(case):
+    """Trace of a golden case: inline arrays or (spec, seed) via our generator."""
+    if case.get("trace") is not None:
+        return {k: np.asarray(v, dtype=np.float64) for k, v in case["trace"].items()}
+    return eng.generate_trace(case["trace_spec"], case["seed"])

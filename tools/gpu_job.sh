@@ -1,0 +1,23 @@
+#!/bin/bash
+# One GPU session: parity tests, the benchmark line, ncu launch list and full
+# captures of the two graded kernels.  Usage: tools/gpu_job.sh [tests] [bench] [ncu]
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+what="${*:-tests bench ncu}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu.txt 2>&1
+if [[ $what == *tests* ]]; then
+  timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+  tail -5 gpurun_out/pytest_gpu.log
+fi
+if [[ $what == *bench* ]]; then
+  timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+  tail -c 3000 gpurun_out/bench.json
+fi
+if [[ $what == *ncu* ]]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv \
+      python tools/perf_probe.py C2 - 1 > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+      -k regex:k_simILi32ELi1ELb0 -c 1 -o gpurun_out/prof_k4_c2 -f python tools/perf_probe.py C2 - 1 > gpurun_out/ncu_k4.log 2>&1; echo "ncu k4 rc=$?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_route_aggregate -s 1 -c 1 \
+      -o gpurun_out/prof_k1_c5 -f python tools/k1_probe.py C5 > gpurun_out/ncu_k1.log 2>&1; echo "ncu k1 rc=$?"
+fi
