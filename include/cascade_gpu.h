@@ -146,6 +146,8 @@ typedef struct cg_sweep_stats {
     int64_t plans_stable;         /* plans passing the stability filter */
     int64_t plans_simulated_full; /* 2000-request simulations run to completion */
     int64_t plans_pruned;         /* simulations stopped by the exact p95 bound */
+    int64_t plans_bound_skipped;  /* excluded by the exact service-time bound, unsimulated */
+    int64_t plans_seeded;         /* bound-seeding simulations (re-visited by the sweep) */
     int64_t plans_overflow;       /* re-run by the deep-queue kernel */
     int64_t request_steps;        /* JSQ dispatch steps executed */
     int64_t h2d_bytes;

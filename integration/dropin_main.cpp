@@ -1,0 +1,89 @@
+// Drop-in check: the reference planner with cascade::outerplan::sweep served
+// by the GPU engine (integration/outerplan_gpu.cpp) vs. the reference's own
+// CPU body (outerplan.cpp compiled with -Dsweep=cpu_sweep, see
+// oracle/Makefile target `dropin`).  Runs the CLI's plan pipeline and
+// compares the output files byte for byte.
+//
+//   dropin_check <config.json> <trace-spec.json> <seed> <out_dir> [min_quality]
+//
+// Writes <out_dir>/{gpu,cpu}/{plan.json,front.json,front.csv,sweep.json} and
+// prints one JSON line {"identical": bool, "files": {...}, "gpu_s":..,"cpu_s":..}.
+#include <chrono>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+
+#include "cascade/cli.hpp"
+#include "cascade/outerplan.hpp"
+
+namespace cascade::outerplan {
+SweepResult cpu_sweep(const std::vector<TraceRecord>& trace, const std::vector<ModelSpec>& models,
+                      const HardwareSpec& hw, const costmodel::CostModelParams& params, int total_gpus,
+                      const SweepConfig& cfg);
+}
+
+using namespace cascade;
+using nlohmann::json;
+
+static std::string slurp(const std::string& p) {
+    std::ifstream in(p);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+
+int main(int argc, char** argv) {
+    if (argc < 5) {
+        std::fprintf(stderr, "usage: %s config.json spec.json seed out_dir [min_quality]\n", argv[0]);
+        return 2;
+    }
+    const std::string cfg_path = argv[1], spec_path = argv[2], out = argv[4];
+    const uint64_t seed = std::stoull(argv[3]);
+    const double min_q = argc > 5 ? std::stod(argv[5]) : 0.0;
+    namespace fs = std::filesystem;
+    fs::create_directories(out + "/gpu");
+    fs::create_directories(out + "/cpu");
+    auto spec = json::parse(slurp(spec_path)).get<cli::TraceGenSpec>();
+    auto trace = cli::generate_trace(spec, seed);
+    const std::string trace_path = out + "/trace.jsonl";
+    write_trace_jsonl(trace_path, trace);
+
+    // GPU: the reference CLI pipeline, whose sweep() call now lands in the engine.
+    cli::PlanArgs args;
+    args.config_path = cfg_path;
+    args.trace_path = trace_path;
+    args.out_dir = out + "/gpu";
+    args.min_quality = min_q;
+    auto t0 = std::chrono::steady_clock::now();
+    cli::cmd_plan(args);
+    const double gpu_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+    // CPU: the reference's own sweep body, same writers as cmd_plan.
+    auto cfg = cli::load_planner_config(cfg_path);
+    auto tr = read_trace_jsonl(trace_path);
+    t0 = std::chrono::steady_clock::now();
+    auto res = outerplan::cpu_sweep(tr, cfg.models, cfg.hardware, cfg.cost_model, cfg.hardware.gpu_count, cfg.sweep);
+    const double cpu_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    outerplan::PlanRequirement req;
+    req.min_quality = min_q;
+    auto plan = outerplan::select_plan(res.front, req);
+    cli::write_output_file(out + "/cpu", "plan.json", json(plan).dump(2) + "\n");
+    cli::write_output_file(out + "/cpu", "front.json", json(res.front).dump(2) + "\n");
+    cli::write_output_file(out + "/cpu", "front.csv", outerplan::front_to_csv(res.front));
+    cli::write_output_file(out + "/cpu", "sweep.json", json(res).dump(2) + "\n");
+
+    json report;
+    bool all = true;
+    for (const char* f : {"plan.json", "front.json", "front.csv", "sweep.json"}) {
+        const std::string a = slurp(out + "/gpu/" + f), b = slurp(out + "/cpu/" + f);
+        report["files"][f] = {{"identical", a == b}, {"bytes", a.size()}};
+        all = all && a == b;
+    }
+    report["identical"] = all;
+    report["gpu_s"] = gpu_s;
+    report["cpu_s"] = cpu_s;
+    std::cout << report.dump() << std::endl;
+    return all ? 0 : 1;
+}

@@ -88,10 +88,14 @@ struct RowSetupArgs {
     RowTables tab;
 };
 
-enum : int { CTR_STABLE = 0, CTR_FULL = 1, CTR_PRUNED = 2, CTR_STEPS = 3, CTR_COUNT = 8 };
+enum : int { CTR_STABLE = 0, CTR_FULL = 1, CTR_PRUNED = 2, CTR_STEPS = 3, CTR_BOUND = 4, CTR_SEED = 5,
+             CTR_COUNT = 8 };
+enum : int { SIM_RANGE = 0, SIM_LIST = 1, SIM_DEEP = 2 };
 
 struct SimArgs {
     int N, n_req, K, prune, item_plans;
+    int dp_lo, dp_hi;                          // SIM_RANGE: plans with dp in (dp_lo, dp_hi]
+    int kstar;                                 // index of the K-th largest CRN output
     int nrows;                                 // rows of this class
     const int* row_ids;                        // class rows -> global row index
     const unsigned long long* item_prefix;     // [nrows+1] cumulative item counts
@@ -122,9 +126,10 @@ struct SimGeometry {
 
 int class_for_dp(int dpmax);
 void class_shape(int cls, int* W, int* R);
-SimGeometry sim_geometry(int cls, bool deep, int sm_count);
+void class_dp_range(int cls, int* lo, int* hi);
+SimGeometry sim_geometry(int cls, int mode, int sm_count);
 void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches);
-void launch_sim(const SimArgs& a, int cls, bool deep, int sm_count, cudaStream_t s, int* launches,
+void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out);
 
 struct ResolveArgs {

@@ -160,7 +160,7 @@ struct cg_engine {
     DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
     DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
-        d_scratch, d_ring, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
+        d_scratch, d_ring, d_seeds, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_acc;
 };
@@ -284,24 +284,92 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     CG_CUDA(cudaMemsetAsync(ctrs, 0, 8 * CTR_COUNT, x.s));
 
     const int K = n_req - (int)p95_index(n_req);
+    // index of the K-th largest CRN output: outputs are monotone in -L[2k+1]
+    int kstar = 0;
+    {
+        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
+        std::vector<int> idx(n_req);
+        for (int k = 0; k < n_req; ++k) idx[k] = k;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
+        kstar = idx[K - 1];
+    }
+    // Every row is simulated by the kernels of each replica-count class its
+    // plans can fall in (lane width W matched to the plan's replica count).
     std::map<int, std::vector<int>> by_cls;
     for (int r = 0; r < nrows; ++r) {
         const auto& sp = hs[rows[r].space];
         x.st.plans_enumerated += (long long)sp.num_plans;
         if (sp.num_plans == 0 || N < 1) continue;
-        by_cls[rows[r].cls].push_back(r);
+        const int dpmax = N / sp.min_gpus;
+        for (int cls = 0; cls < 7; ++cls) {
+            int lo, hi;
+            class_dp_range(cls, &lo, &hi);
+            if (lo < dpmax) by_cls[cls].push_back(r);
+        }
     }
     long long max_slots = 1;
     for (auto& kv : by_cls) {
-        SimGeometry g = sim_geometry(kv.first, false, E.sm_count);
-        SimGeometry gd = sim_geometry(kv.first, true, E.sm_count);
+        SimGeometry g = sim_geometry(kv.first, SIM_RANGE, E.sm_count);
+        SimGeometry gd = sim_geometry(kv.first, SIM_DEEP, E.sm_count);
         max_slots = std::max({max_slots, g.slots, gd.slots});
     }
+    max_slots = std::max(max_slots, sim_geometry(3, SIM_LIST, E.sm_count).slots);
     double* scratch = E.d_scratch.as<double>((size_t)max_slots * n_req);
     int ring_cap = 1;
     while (ring_cap < n_req) ring_cap <<= 1;
 
+    SimArgs base{};
+    base.N = N;
+    base.n_req = n_req;
+    base.K = K;
+    base.kstar = kstar;
+    base.prune = E.prune;
+    base.item_counter = ictr;
+    base.rows = static_cast<RowDesc*>(E.d_rows.p);
+    base.spaces = static_cast<PlanSpace*>(E.d_spaces.p);
+    base.tab = tab;
+    base.lat_min = latmin;
+    base.ub = ub;
+    base.ties = ties;
+    base.tie_count = tiecnt;
+    base.tie_cap = (unsigned long long)E.tie_cap;
+    base.ovf = ovf;
+    base.ovf_count = ovfcnt;
+    base.ovf_cap = (unsigned long long)E.ovf_cap;
+    base.scratch = scratch;
+    base.counters = ctrs;
+    base.ring_cap = ring_cap;
+
     CG_CUDA(cudaEventRecord(E.ev[8], x.s));
+    // Bound seeding: homogeneous plans (c replicas of one shape) of the heavy
+    // rows first, so the exact pruning bound is tight from the start.  Seeds
+    // are re-visited by the range kernels (idempotent), so this only moves work.
+    if (E.prune && E.world == 1) {
+        std::vector<SimItem> seeds;
+        for (int r = 0; r < nrows; ++r) {
+            const auto& sp = hs[rows[r].space];
+            if (sp.num_plans < 4096 || N < 1) continue;
+            const int S = (int)sp.shapes.size();
+            for (int sidx = 0; sidx < S; ++sidx)
+                for (int c = 1; c * sp.shapes[sidx].gpus <= N && c <= 32; ++c) {
+                    // rank of the count vector (c at sidx, zeros elsewhere)
+                    unsigned long long q = 0;
+                    int b = N;
+                    for (int k = 0; k < c; ++k) q += sp.w(sidx + 1, b - k * sp.shapes[sidx].gpus);
+                    seeds.push_back(SimItem{r, 0, q - 1, q});
+                }
+        }
+        if (!seeds.empty()) {
+            SimItem* dseeds = E.d_seeds.as<SimItem>(seeds.size());
+            x.h2d(dseeds, seeds.data(), seeds.size() * sizeof(SimItem));
+            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
+            CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
+            SimArgs a = base;
+            a.deep_items = dseeds;
+            a.nitems = seeds.size();
+            launch_sim(a, 3, SIM_LIST, E.sm_count, x.s, &x.launches, nullptr);
+        }
+    }
     for (auto& kv : by_cls) {
         const int cls = kv.first;
         const auto& rl = kv.second;
@@ -309,7 +377,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         // group slot of the persistent grid gets >= ~16 items
         unsigned long long class_plans = 0;
         for (int r : rl) class_plans += hs[rows[r].space].num_plans;
-        const SimGeometry geo = sim_geometry(cls, false, E.sm_count);
+        const SimGeometry geo = sim_geometry(cls, SIM_RANGE, E.sm_count);
         const unsigned long long per =
             std::max<unsigned long long>(1ull, class_plans / ((unsigned long long)geo.slots * 16ull));
         const int item_plans = (int)std::min<unsigned long long>((unsigned long long)E.item_plans,
@@ -330,39 +398,21 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         x.h2d(ictr, &lo, 8);
         CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
 
-        SimArgs a{};
-        a.N = N;
-        a.n_req = n_req;
-        a.K = K;
-        a.prune = E.prune;
+        SimArgs a = base;
         a.item_plans = item_plans;
+        class_dp_range(cls, &a.dp_lo, &a.dp_hi);
         a.nrows = (int)rl.size();
         a.row_ids = rowids;
         a.item_prefix = ipre;
         a.nitems = hi;
-        a.item_counter = ictr;
-        a.rows = static_cast<RowDesc*>(E.d_rows.p);
-        a.spaces = static_cast<PlanSpace*>(E.d_spaces.p);
-        a.tab = tab;
-        a.lat_min = latmin;
-        a.ub = ub;
-        a.ties = ties;
-        a.tie_count = tiecnt;
-        a.tie_cap = (unsigned long long)E.tie_cap;
-        a.ovf = ovf;
-        a.ovf_count = ovfcnt;
-        a.ovf_cap = (unsigned long long)E.ovf_cap;
-        a.scratch = scratch;
-        a.counters = ctrs;
-        a.ring_cap = ring_cap;
-        if (hi > lo) launch_sim(a, cls, false, E.sm_count, x.s, &x.launches, nullptr);
+        if (hi > lo) launch_sim(a, cls, SIM_RANGE, E.sm_count, x.s, &x.launches, nullptr);
         unsigned long long novf = 0;
         x.d2h(&novf, ovfcnt, 8);
         x.sync();
         if (novf > (unsigned long long)E.ovf_cap) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
         x.st.plans_overflow += (long long)novf;
         if (novf > 0) {  // deep-queue re-runs (rings in global memory, capacity >= n_req)
-            SimGeometry gd = sim_geometry(cls, true, E.sm_count);
+            SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
             double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
             CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
             CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
@@ -371,7 +421,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             d.nitems = novf;
             d.ring_global = ring;
             d.ovf_count = ovfcnt2;
-            launch_sim(d, cls, true, E.sm_count, x.s, &x.launches, nullptr);
+            launch_sim(d, cls, SIM_DEEP, E.sm_count, x.s, &x.launches, nullptr);
         }
     }
     CG_CUDA(cudaEventRecord(E.ev[9], x.s));
@@ -387,6 +437,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     x.st.plans_stable += (long long)h_ctr[CTR_STABLE];
     x.st.plans_simulated_full += (long long)h_ctr[CTR_FULL];
     x.st.plans_pruned += (long long)h_ctr[CTR_PRUNED];
+    x.st.plans_bound_skipped += (long long)h_ctr[CTR_BOUND];
+    x.st.plans_seeded += (long long)h_ctr[CTR_SEED];
     x.st.request_steps += (long long)h_ctr[CTR_STEPS];
 
     unsigned long long* best = E.d_best.as<unsigned long long>(cells);
@@ -877,7 +929,7 @@ cg_status cg_sweep(cg_engine* E, const cg_trace* tr, const cg_model* models, int
                 RowDesc rd{};
                 rd.stage = i;
                 rd.space = i;
-                rd.cls = row_class(hs[i], N);
+                rd.cls = 0;
                 rd.dpmax = hs[i].min_gpus > 0 ? N / hs[i].min_gpus : 0;
                 rd.rate = R.stats[(size_t)w * 5 + 0];
                 rd.mean_in = R.stats[(size_t)w * 5 + 1];
@@ -1195,7 +1247,7 @@ cg_status cg_stage_row(cg_engine* E, const cg_model* model, const cg_workload* w
             cg_model m = *model;
             auto hs = build_spaces(x, &m, 1, *hw, *q, N);
             std::vector<RowDesc> rows(1);
-            rows[0] = RowDesc{0, 0, row_class(hs[0], N), hs[0].min_gpus > 0 ? N / hs[0].min_gpus : 0,
+            rows[0] = RowDesc{0, 0, 0, hs[0].min_gpus > 0 ? N / hs[0].min_gpus : 0,
                               ws[0], ws[1], ws[2], ws[3], ws[4]};
             evaluate_rows(x, rows, hs, *hw, *q, N);
             std::vector<double> lat(N + 1);

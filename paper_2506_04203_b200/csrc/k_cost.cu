@@ -127,16 +127,24 @@ struct GroupShared {
     int dp;
     int status;
     int has_item;
-    int pad;
+    int dp_enum;  // replicas of the current count vector
     unsigned char counts[kMaxShapes];
-    unsigned hist[256];
 };
 
-template <int W, int R, bool DEEP>
+// MODE: 0 = plan-index ranges (smem rings), 1 = explicit plan list (smem
+// rings; bound seeding), 2 = explicit list with global-memory rings (deep
+// re-runs of ring overflows).
+enum : int { MODE_RANGE = 0, MODE_LIST = 1, MODE_DEEP = 2 };
+
+template <int W, int R, int MODE>
 struct Traits {
+    static constexpr bool DEEP = MODE == MODE_DEEP;
     static constexpr int G = 32 / W;
     static constexpr int CAP = R == 1 ? 32 : (R == 2 ? 16 : 8);
-    static constexpr size_t ring_bytes_per_warp = DEEP ? 0 : (size_t)32 * R * CAP * sizeof(double);
+    // non-DEEP: the finished group's ring columns double as its radix-select
+    // histogram (W*R*CAP*2 >= 256 words); DEEP keeps a 256-word histogram.
+    static constexpr size_t ring_bytes_per_warp = DEEP ? 256 * sizeof(unsigned)
+                                                       : (size_t)32 * R * CAP * sizeof(double);
     static constexpr size_t bytes_per_warp = ring_bytes_per_warp + G * sizeof(GroupShared);
 };
 
@@ -144,15 +152,18 @@ __device__ __forceinline__ void count_add(unsigned long long* ctr, unsigned long
     if (v) atomicAdd(ctr, v);
 }
 
-// Leader lane: advance to the next stable plan (or mark the group done).
-template <bool DEEP>
+// Leader lane: advance to the next plan of this kernel's dp class that is
+// stable (costmodel.cpp:366-376) and not excluded by the exact service-time
+// bound; or mark the group done.
+template <int MODE>
 __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
     while (true) {
         if (gs.has_item && gs.plan + 1 < gs.hi) {
             const PlanSpace& sp = a.spaces[a.rows[gs.row].space];
-            int used = gs.used;
-            next_plan(sp, gs.counts, used);
+            int used = gs.used, dpe = gs.dp_enum;
+            next_plan(sp, gs.counts, used, dpe);
             gs.used = used;
+            gs.dp_enum = dpe;
             gs.plan += 1;
         } else {
             const unsigned long long it = atomicAdd(a.item_counter, 1ull);
@@ -163,7 +174,7 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
             }
             int row;
             unsigned long long lo, hi;
-            if (DEEP) {
+            if (MODE != MODE_RANGE) {
                 const SimItem si = a.deep_items[it];
                 row = si.row;
                 lo = si.lo;
@@ -185,16 +196,21 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
             gs.plan = lo;
             gs.hi = hi;
             gs.has_item = 1;
-            gs.used = unrank_plan(a.spaces[a.rows[row].space], lo, gs.counts);
+            const PlanSpace& sp = a.spaces[a.rows[row].space];
+            gs.used = unrank_plan(sp, lo, gs.counts);
+            int dpe = 0;
+            for (int s = 0; s < sp.S; ++s) dpe += gs.counts[s];
+            gs.dp_enum = dpe;
         }
-        // stability filter (costmodel.cpp:366-376), parts order = ascending shape
+        // this kernel simulates only its replica-count class (lane width W)
+        if (MODE == MODE_RANGE && (gs.dp_enum <= a.dp_lo || gs.dp_enum > a.dp_hi)) continue;
         const RowDesc& rd = a.rows[gs.row];
         const PlanSpace& sp = a.spaces[rd.space];
-        const unsigned char* ok = a.tab.shape_ok + (long long)gs.row * kMaxShapes;
-        const double* ms = a.tab.mean_service + (long long)gs.row * kMaxShapes;
+        const long long rb = (long long)gs.row * kMaxShapes;
+        const unsigned char* ok = a.tab.shape_ok + rb;
+        const double* ms = a.tab.mean_service + rb;
         bool good = true;
         double capacity = 0.0;
-        int dp = 0;
         for (int s = 0; s < sp.S; ++s) {
             const int c = gs.counts[s];
             if (!c) continue;
@@ -203,11 +219,34 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
                 break;
             }
             capacity = __dadd_rn(capacity, __ddiv_rn((double)c, ms[s]));
-            dp += c;
         }
         if (!good || rd.rate >= capacity) continue;
-        if (!DEEP) atomicAdd(&a.counters[CTR_STABLE], 1ull);
-        gs.dp = dp;
+        if (MODE == MODE_RANGE) atomicAdd(&a.counters[CTR_STABLE], 1ull);
+        if (a.prune && MODE != MODE_DEEP) {
+            // Exact bound without simulation: every sojourn on shape s is >=
+            // fl(fl(fl(t+p_s)+fl(o d_s))-t) >= (p_s+o d_s)(1-5u) - 2u t, and
+            // min_s(p_s + o d_s) is increasing in o, so the K-th largest sojourn
+            // is >= min_{s in plan}(p_s + o_(K) d_s)(1-1e-12) - 1e-12 T_max,
+            // o_(K) = the K-th largest CRN output (index kstar).  A plan whose
+            // bound exceeds the best latency already found at <= its budget can
+            // never enter the row.
+            const double o_k = a.tab.O[(long long)gs.row * a.n_req + a.kstar];
+            const double t_max = a.tab.T[(long long)gs.row * a.n_req + a.n_req - 1];
+            double lb = __longlong_as_double(0x7ff0000000000000ll);
+            for (int s = 0; s < sp.S; ++s) {
+                if (!gs.counts[s]) continue;
+                const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
+                lb = v < lb ? v : lb;
+            }
+            lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
+            const double U = __longlong_as_double(
+                (long long)*(volatile unsigned long long*)&a.ub[(long long)gs.row * (a.N + 1) + gs.used]);
+            if (lb > U) {
+                atomicAdd(&a.counters[CTR_BOUND], 1ull);
+                continue;
+            }
+        }
+        gs.dp = gs.dp_enum;
         gs.status = ST_RUN;
         return;
     }
@@ -215,7 +254,15 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
 
 // Group-cooperative exact K-th largest of n non-negative doubles (8-bit
 // radix select on the IEEE bit patterns, constant bytes skipped).
-template <int W>
+// hist word b of a group: contiguous 256 words (DEEP) or the group's ring
+// columns (slot-major, W lanes x 2 words per slot).
+template <int W, bool CONTIG>
+__device__ __forceinline__ unsigned* hword(unsigned* base, int gshift, int b) {
+    if (CONTIG) return base + b;
+    return base + ((b / (2 * W)) * 32 + gshift) * 2 + (b % (2 * W));
+}
+
+template <int W, bool CONTIG>
 __device__ unsigned long long group_kth_largest(const double* __restrict__ buf, int n, int K, int gl,
                                                 unsigned gm, int gshift, unsigned* hist) {
     unsigned long long o = 0, an = ~0ull;
@@ -240,18 +287,18 @@ __device__ unsigned long long group_kth_largest(const double* __restrict__ buf, 
             pmask |= dm;
             continue;
         }
-        for (int b = gl; b < 256; b += W) hist[b] = 0;
+        for (int b = gl; b < 256; b += W) *hword<W, CONTIG>(hist, gshift, b) = 0;
         __syncwarp(gm);
         for (int i = gl; i < n; i += W) {
             const unsigned long long k = (unsigned long long)__double_as_longlong(buf[i]);
-            if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255ull], 1u);
+            if ((k & pmask) == prefix) atomicAdd(hword<W, CONTIG>(hist, gshift, (int)((k >> shift) & 255ull)), 1u);
         }
         __syncwarp(gm);
         constexpr int B = 256 / W;
         const int top = 255 - gl * B;
         int seg = 0;
-#pragma unroll
-        for (int j = 0; j < B; ++j) seg += hist[top - j];
+#pragma unroll 4
+        for (int j = 0; j < B; ++j) seg += *hword<W, CONTIG>(hist, gshift, top - j);
         int incl = seg;
 #pragma unroll
         for (int off = 1; off < W; off <<= 1) {
@@ -263,7 +310,7 @@ __device__ unsigned long long group_kth_largest(const double* __restrict__ buf, 
         int digit = 0, before = 0;
         if (mine) {
             for (int j = 0; j < B; ++j) {
-                const int c = hist[top - j];
+                const int c = *hword<W, CONTIG>(hist, gshift, top - j);
                 if (excl + c >= need) {
                     digit = top - j;
                     before = excl;
@@ -284,9 +331,11 @@ __device__ unsigned long long group_kth_largest(const double* __restrict__ buf, 
     return prefix;
 }
 
-template <int W, int R, bool DEEP>
-__global__ void __launch_bounds__(128) k_sim(SimArgs a) {
-    using TR = Traits<W, R, DEEP>;
+template <int W, int R, int MODE>
+__global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
+    using TR = Traits<W, R, MODE>;
+    constexpr bool DEEP = TR::DEEP;
+    constexpr int UNROLL = 4;
     constexpr int G = TR::G;
     constexpr int CAP = TR::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -321,8 +370,8 @@ __global__ void __launch_bounds__(128) k_sim(SimArgs a) {
     unsigned long long plan = 0;
     bool ovf = false;
     double U = __longlong_as_double((long long)kInfBits);
-    const double* Trow = nullptr;
-    const double* Orow = nullptr;
+    const double* Trow = a.tab.T;  // valid dummies until a plan is acquired
+    const double* Orow = a.tab.O;
     double nd[R], avail[R], pre[R], dec[R];
     int cnt[R], head[R], tail[R];
 #pragma unroll
@@ -337,7 +386,7 @@ __global__ void __launch_bounds__(128) k_sim(SimArgs a) {
         // ---- phase A: groups without a plan acquire one
         const bool need = status == ST_NEED;
         if (__any_sync(FULL, need)) {
-            if (need && gl == 0) acquire_plan<DEEP>(a, gs);
+            if (need && gl == 0) acquire_plan<MODE>(a, gs);
             __syncwarp();
             if (need) {
                 status = gs.status;
@@ -376,83 +425,83 @@ __global__ void __launch_bounds__(128) k_sim(SimArgs a) {
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
 
-        // ---- phase B: one JSQ dispatch step per running group
-        const bool run = status == ST_RUN;
-        double t = 0.0, o = 0.0;
-        if (run) {
-            t = __ldg(&Trow[k]);
-            o = __ldg(&Orow[k]);
-        }
+        // ---- phase B: UNROLL JSQ dispatch steps per running group.  The
+        // winner's update is predicated (no divergent branch); only the rare
+        // all-busy case takes the butterfly-min path.
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            while (nd[r] <= t && run) {  // departures up to t (fin <= t has left)
-                --cnt[r];
-                if (cnt[r] > 0) {
-                    const int slotr = head[r] & ring_mask;
-                    nd[r] = DEEP ? gring[((long long)r * ring_cap + slotr) * 32 + lane]
-                                 : ring[(r * CAP + slotr) * 32 + lane];
-                    ++head[r];
-                } else {
-                    nd[r] = INF;
-                }
-            }
-        }
-        int win = -1;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const bool idle = run && cnt[r] == 0 && (r * W + gl) < dp;
-            const unsigned gb = (__ballot_sync(FULL, idle) >> gshift) & wmask;
-            if (win < 0 && gb) win = r * W + (__ffs(gb) - 1);
-        }
-        const bool all_busy = run && win < 0;
-        if (__any_sync(FULL, all_busy)) {
-            unsigned key = 0xffffffffu;
+        for (int u = 0; u < UNROLL; ++u) {
+            const bool run = status == ST_RUN;
+            const int kk = run ? k : 0;
+            const double t = __ldg(&Trow[kk]);
+            const double o = __ldg(&Orow[kk]);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int j = r * W + gl;
-                if (j < dp) {
-                    const unsigned kk = ((unsigned)cnt[r] << 9) | (unsigned)j;
-                    key = kk < key ? kk : key;
-                }
-            }
-#pragma unroll
-            for (int off = W / 2; off > 0; off >>= 1) {
-                const unsigned v = __shfl_xor_sync(FULL, key, off);
-                key = v < key ? v : key;
-            }
-            if (all_busy) win = (int)(key & 511u);
-        }
-        if (run) {
-            if (gl == (win & (W - 1))) {
-                const int wr = win / W;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if (r == wr) {
-                        const double start = (t < avail[r]) ? avail[r] : t;  // std::max(t, avail)
-                        const double fin = __dadd_rn(__dadd_rn(start, pre[r]), __dmul_rn(o, dec[r]));
-                        const double soj = __dsub_rn(fin, t);
-                        if (cnt[r] == 0) {
-                            nd[r] = fin;
-                        } else {
-                            const int slotr = tail[r] & ring_mask;
-                            if (DEEP) gring[((long long)r * ring_cap + slotr) * 32 + lane] = fin;
-                            else ring[(r * CAP + slotr) * 32 + lane] = fin;
-                            ++tail[r];
-                            if (tail[r] - head[r] > ring_cap) ovf = true;
-                        }
-                        ++cnt[r];
-                        avail[r] = fin;
-                        scratch[k] = soj;
-                        ab += (soj > U) ? 1 : 0;
+                while (run && nd[r] <= t) {  // departures up to t (fin <= t has left)
+                    --cnt[r];
+                    if (cnt[r] > 0) {
+                        const int slotr = head[r] & ring_mask;
+                        nd[r] = DEEP ? gring[((long long)r * ring_cap + slotr) * 32 + lane]
+                                     : ring[(r * CAP + slotr) * 32 + lane];
+                        ++head[r];
+                    } else {
+                        nd[r] = INF;
                     }
                 }
             }
-            ++k;
-            if (k == a.n_req) status = ST_FINISH;
+            int win = -1;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool idle = run && cnt[r] == 0 && (r * W + gl) < dp;
+                const unsigned gb = (__ballot_sync(FULL, idle) >> gshift) & wmask;
+                if (win < 0 && gb) win = r * W + (__ffs(gb) - 1);
+            }
+            const bool all_busy = run && win < 0;
+            if (__any_sync(FULL, all_busy)) {
+                unsigned key = 0xffffffffu;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int j = r * W + gl;
+                    if (j < dp) {
+                        const unsigned kk2 = ((unsigned)cnt[r] << 9) | (unsigned)j;
+                        key = kk2 < key ? kk2 : key;
+                    }
+                }
+#pragma unroll
+                for (int off = W / 2; off > 0; off >>= 1) {
+                    const unsigned v = __shfl_xor_sync(FULL, key, off);
+                    key = v < key ? v : key;
+                }
+                if (all_busy) win = (int)(key & 511u);
+            }
+            const int wl = win & (W - 1), wr = win / W;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool me = run && gl == wl && r == wr;
+                const double start = (t < avail[r]) ? avail[r] : t;  // std::max(t, avail)
+                const double fin = __dadd_rn(__dadd_rn(start, pre[r]), __dmul_rn(o, dec[r]));
+                const double soj = __dsub_rn(fin, t);
+                const bool push = me && cnt[r] > 0;
+                if (push) {
+                    const int slotr = tail[r] & ring_mask;
+                    if (DEEP) gring[((long long)r * ring_cap + slotr) * 32 + lane] = fin;
+                    else ring[(r * CAP + slotr) * 32 + lane] = fin;
+                }
+                if (me && cnt[r] == 0) nd[r] = fin;
+                tail[r] += push ? 1 : 0;
+                ovf |= push && (tail[r] - head[r] > ring_cap);
+                cnt[r] += me ? 1 : 0;
+                avail[r] = me ? fin : avail[r];
+                if (me) scratch[kk] = soj;
+                ab += (me && soj > U) ? 1 : 0;
+            }
+            if (run) {
+                ++k;
+                if (k == a.n_req) status = ST_FINISH;
+            }
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
-        if ((it & 31u) == 31u) {
+        if ((it & (32u / UNROLL - 1u)) == (32u / UNROLL - 1u)) {
             int tot = ab;
             int ov = ovf ? 1 : 0;
 #pragma unroll
@@ -500,8 +549,8 @@ __global__ void __launch_bounds__(128) k_sim(SimArgs a) {
                     pruned += 1;
                 } else {
                     __syncwarp(gm);
-                    const unsigned long long xb =
-                        group_kth_largest<W>(scratch, a.n_req, a.K, gl, gm, gshift, gs.hist);
+                    const unsigned long long xb = group_kth_largest<W, DEEP>(
+                        scratch, a.n_req, a.K, gl, gm, gshift, reinterpret_cast<unsigned*>(wbase));
                     full += 1;
                     if (gl == 0) {
                         const long long base = (long long)row * (a.N + 1);
@@ -526,8 +575,8 @@ __global__ void __launch_bounds__(128) k_sim(SimArgs a) {
     // per-lane counters -> global (leaders only to avoid double counting)
     if (gl == 0) {
         count_add(&a.counters[CTR_STEPS], steps);
-        count_add(&a.counters[CTR_FULL], full);
-        count_add(&a.counters[CTR_PRUNED], pruned);
+        count_add(&a.counters[MODE == MODE_LIST ? CTR_SEED : CTR_FULL], full);
+        count_add(&a.counters[MODE == MODE_LIST ? CTR_SEED : CTR_PRUNED], pruned);
     }
 }
 
@@ -580,17 +629,17 @@ __global__ void k_row_prefix(ResolveArgs a) {
     }
 }
 
-template <int W, int R, bool DEEP>
+template <int W, int R, int MODE>
 void launch_sim_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches, int* grid_out) {
-    using TR = Traits<W, R, DEEP>;
+    using TR = Traits<W, R, MODE>;
     const size_t smem = TR::bytes_per_warp * 4;
-    auto kern = k_sim<W, R, DEEP>;
+    auto kern = k_sim<W, R, MODE>;
     CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     if (per_sm < 1) per_sm = 1;
     int grid = sm_count * per_sm;
-    if (DEEP && grid > sm_count) grid = sm_count;
+    if (MODE == MODE_DEEP && grid > sm_count) grid = sm_count;
     if (grid_out) *grid_out = grid;
     if (a.nitems == 0) return;
     kern<<<grid, 128, smem, s>>>(a);
@@ -600,19 +649,19 @@ void launch_sim_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches,
 
 }  // namespace
 
-SimGeometry sim_geometry(int cls, bool deep, int sm_count) {
+SimGeometry sim_geometry(int cls, int mode, int sm_count) {
     // must mirror launch_sim's grid choice: slots = grid * 4 warps * G
     SimGeometry g{};
     int W = 32, R = 1;
     class_shape(cls, &W, &R);
-    if (deep) W = 32;
+    if (mode != MODE_RANGE) W = 32;
     g.W = W;
     g.R = R;
     g.G = 32 / W;
     int grid = 0;
     SimArgs dummy{};
     dummy.nitems = 0;
-    launch_sim(dummy, cls, deep, sm_count, nullptr, nullptr, &grid);
+    launch_sim(dummy, cls, mode, sm_count, nullptr, nullptr, &grid);
     g.grid = grid;
     g.slots = (long long)grid * 4 * g.G;
     g.warps = (long long)grid * 4;
@@ -626,6 +675,12 @@ void class_shape(int cls, int* W, int* R) {
     *R = Rs[cls];
 }
 
+void class_dp_range(int cls, int* lo, int* hi) {
+    static const int His[7] = {4, 8, 16, 32, 64, 128, 256};
+    *lo = cls == 0 ? 0 : His[cls - 1];
+    *hi = His[cls];
+}
+
 int class_for_dp(int dpmax) {
     if (dpmax <= 4) return 0;
     if (dpmax <= 8) return 1;
@@ -637,24 +692,29 @@ int class_for_dp(int dpmax) {
     return -1;
 }
 
-void launch_sim(const SimArgs& a, int cls, bool deep, int sm_count, cudaStream_t s, int* launches,
+void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out) {
-    if (deep) {
+    if (mode == MODE_DEEP) {
         switch (cls) {
-            case 0: case 1: case 2: case 3: launch_sim_t<32, 1, true>(a, sm_count, s, launches, grid_out); return;
-            case 4: launch_sim_t<32, 2, true>(a, sm_count, s, launches, grid_out); return;
-            case 5: launch_sim_t<32, 4, true>(a, sm_count, s, launches, grid_out); return;
-            case 6: launch_sim_t<32, 8, true>(a, sm_count, s, launches, grid_out); return;
+            case 0: case 1: case 2: case 3: launch_sim_t<32, 1, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
+            case 5: launch_sim_t<32, 4, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
+            case 6: launch_sim_t<32, 8, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
+        }
+    } else if (mode == MODE_LIST) {
+        switch (cls) {
+            case 0: case 1: case 2: case 3: launch_sim_t<32, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
         }
     } else {
         switch (cls) {
-            case 0: launch_sim_t<4, 1, false>(a, sm_count, s, launches, grid_out); return;
-            case 1: launch_sim_t<8, 1, false>(a, sm_count, s, launches, grid_out); return;
-            case 2: launch_sim_t<16, 1, false>(a, sm_count, s, launches, grid_out); return;
-            case 3: launch_sim_t<32, 1, false>(a, sm_count, s, launches, grid_out); return;
-            case 4: launch_sim_t<32, 2, false>(a, sm_count, s, launches, grid_out); return;
-            case 5: launch_sim_t<32, 4, false>(a, sm_count, s, launches, grid_out); return;
-            case 6: launch_sim_t<32, 8, false>(a, sm_count, s, launches, grid_out); return;
+            case 0: launch_sim_t<4, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 1: launch_sim_t<8, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 2: launch_sim_t<16, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 3: launch_sim_t<32, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 5: launch_sim_t<32, 4, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 6: launch_sim_t<32, 8, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
         }
     }
     throw EngineError(101, "unsupported JSQ kernel class");

@@ -35,16 +35,19 @@ __device__ inline int unrank_plan(const PlanSpace& sp, unsigned long long p, uns
     return used;
 }
 
-// successor in the recursion order (last shape fastest); false at the end
-__device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& used) {
+// successor in the recursion order (last shape fastest); false at the end.
+// `used` (GPUs) and `dp` (replicas) are maintained incrementally.
+__device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& used, int& dp) {
     for (int i = sp.S - 1; i >= 0; --i) {
         const int size = sp.shapes[i].gpus;
         if (used + size <= sp.N) {
             c[i] = (unsigned char)(c[i] + 1);
             used += size;
+            dp += 1;
             return true;
         }
         used -= c[i] * size;
+        dp -= c[i];
         c[i] = 0;
     }
     return false;

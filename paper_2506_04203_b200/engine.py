@@ -102,7 +102,7 @@ class Plan(ctypes.Structure):
 class SweepStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "candidates", "distinct_candidates", "stage_workloads", "unique_rows", "plans_enumerated",
-        "plans_stable", "plans_simulated_full", "plans_pruned", "plans_overflow", "request_steps",
+        "plans_stable", "plans_simulated_full", "plans_pruned", "plans_bound_skipped", "plans_seeded", "plans_overflow", "request_steps",
         "h2d_bytes", "d2h_bytes")] + [("num_ranks", ctypes.c_int32), ("gpu_launches", ctypes.c_int32)] + \
         [(n, ctypes.c_double) for n in ("ms_total", "ms_route", "ms_quality", "ms_rows", "ms_solve",
                                         "ms_k1", "k1_bytes", "ms_k4")]
