@@ -230,6 +230,24 @@ typedef struct cg_route_result {
 cg_status cg_route(cg_engine* engine, const cg_trace* trace, const double* thresholds,
                    const int32_t* deployed, cg_route_result* out, int32_t* accept_stage);
 
+/* Batched route_trace over every threshold candidate of a grid (all stages
+ * deployed), i.e. the routing phase of sweep on its own (outerplan.cpp:229-234):
+ * per candidate (cartesian order, first dimension outermost) the
+ * RoutingOutcome ratios, stage workloads and quality. */
+typedef struct cg_route_grid_result {
+    int32_t stages;
+    int64_t num_candidates;
+    double* thresholds;   /* [K][C-1] */
+    double* ratios;       /* [K][C] */
+    cg_workload* workloads; /* [K][C] */
+    double* quality;      /* [K] */
+    cg_sweep_stats stats;
+} cg_route_grid_result;
+
+cg_status cg_route_grid(cg_engine* engine, const cg_trace* trace, const cg_sweep_config* cfg,
+                        cg_route_grid_result** out);
+void cg_route_grid_result_free(cg_route_grid_result* result);
+
 /* StageEvaluator::row: latency[f] for f in 0..max_budget (INFINITY when
  * infeasible) and plan_index[f] (-1 = nullopt) into *plans / *replicas. */
 typedef struct cg_row_result {

@@ -24,6 +24,13 @@ struct RouteArgs {
     unsigned long long* ranks;  // [n] packed 16-bit ranks
     unsigned long long* hist;   // [cells][2+C]
     unsigned int* flags;        // bit0: a token is not an integer in [0, 2^32)
+    long long cells;
+    int gtop[4];                   // highest power of two <= G (branch-free rank search)
+    long long marg_off[4];         // word offset of the stage-i output-sum marginal (i < C-1)
+    long long priv_words;          // 3*cells + sum of marginal sizes
+    unsigned long long* partials;  // [blocks][priv_words] block-private histograms (or null)
+    long long max_partials;        // capacity of `partials` in blocks
+    unsigned long long* acc;       // [priv_words] global accumulator (non-private path)
 };
 
 struct WorkloadArgs {

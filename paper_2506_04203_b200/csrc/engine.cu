@@ -160,9 +160,9 @@ struct cg_engine {
     DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
     DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
-        d_scratch, d_ring, d_seeds, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
+        d_scratch, d_ring, d_seeds, d_partials, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_acc;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc;
 };
 
 namespace {
@@ -651,9 +651,26 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
     ra.ranks = E.d_ranks.as<unsigned long long>(n);
     ra.hist = E.d_hist.as<unsigned long long>((size_t)cells * Q);
     ra.flags = E.d_flags.as<unsigned int>(1);
-    CG_CUDA(cudaMemsetAsync(ra.hist, 0, (size_t)cells * Q * 8, x.s));
+    ra.cells = cells;
+    {
+        long long words = 3 * cells;
+        for (int i = 0; i < D; ++i) {  // marginal of stage-i output sums over dims < i
+            ra.marg_off[i] = words;
+            words += (i == 0) ? 1 : ra.stride[i];
+        }
+        ra.priv_words = words;
+        for (int d = 0; d < D; ++d) {
+            int top = 1;
+            while (top * 2 <= ra.G[d]) top *= 2;
+            ra.gtop[d] = ra.G[d] > 0 ? top : 0;
+        }
+    }
+    ra.max_partials = (long long)E.sm_count * 8;
+    ra.partials = (size_t)ra.priv_words * 8 <= 96 * 1024
+                      ? E.d_partials.as<unsigned long long>((size_t)ra.max_partials * ra.priv_words)
+                      : nullptr;
+    ra.acc = E.d_acc.as<unsigned long long>((size_t)ra.priv_words);
     CG_CUDA(cudaMemsetAsync(ra.flags, 0, 4, x.s));
-
     CG_CUDA(cudaEventRecord(E.ev[0], x.s));
     launch_route_aggregate(ra, D, E.sm_count, x.s, &x.launches);
     CG_CUDA(cudaEventRecord(E.ev[1], x.s));
@@ -1203,7 +1220,7 @@ cg_status cg_route(cg_engine* E, const cg_trace* tr, const double* thresholds, c
         if (accept_stage) {
             double* dh = E->d_misc.as<double>(std::max(1, C));
             int* ddep = E->d_dep.as<int>(std::max(1, C));
-            int* dout = E->d_acc.as<int>((size_t)t.n);
+            int* dout = E->d_accept.as<int>((size_t)t.n);
             std::vector<double> hh(thresholds, thresholds + D);
             hh.resize(std::max(1, C), 0.0);
             std::vector<int> dep(deployed, deployed + C);
@@ -1215,6 +1232,95 @@ cg_status cg_route(cg_engine* E, const cg_trace* tr, const double* thresholds, c
             x.sync();
         }
     });
+}
+
+cg_status cg_route_grid(cg_engine* E, const cg_trace* tr, const cg_sweep_config* cfg, cg_route_grid_result** out) {
+    return guarded([&] {
+        Timer timer;
+        if (out) *out = nullptr;
+        if (!E || !tr || !cfg || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        CG_CUDA(cudaSetDevice(E->device));
+        SweepCtx x(*E);
+        if (tr->n <= 0) fail(CG_ERR_EMPTY_TRACE, "route_trace: empty trace");
+        const int C = tr->stages;
+        if (C < 1 || C > kMaxStages) fail(CG_ERR_UNSUPPORTED, "GPU engine supports up to 5 cascade stages");
+        TraceDev t = trace_to_device(x, *tr);
+        const double rate = overall_rate(t);
+        const int D = C - 1;
+        std::vector<std::vector<double>> given;
+        if (cfg->grid_dims == 0) {
+            given = default_grid(x, t);
+        } else {
+            long long off = 0;
+            for (int d = 0; d < cfg->grid_dims; ++d) {
+                given.emplace_back(cfg->grid_values + off, cfg->grid_values + off + cfg->grid_sizes[d]);
+                off += cfg->grid_sizes[d];
+            }
+        }
+        if ((int)given.size() != D) fail(CG_ERR_INVALID_INPUT, "route_trace: thresholds length != C-1");
+        for (const auto& dim : given)
+            if (dim.empty()) fail(CG_ERR_INVALID_INPUT, "sweep: empty threshold grid dimension");
+        std::vector<std::vector<double>> distinct(D);
+        std::vector<std::vector<int>> g2d(D);
+        for (int d = 0; d < D; ++d) {
+            distinct[d] = given[d];
+            std::sort(distinct[d].begin(), distinct[d].end());
+            distinct[d].erase(std::unique(distinct[d].begin(), distinct[d].end()), distinct[d].end());
+            for (double v : given[d])
+                g2d[d].push_back(
+                    (int)(std::lower_bound(distinct[d].begin(), distinct[d].end(), v) - distinct[d].begin()));
+        }
+        RoutingOut R = route_all(x, t, distinct, rate, nullptr);
+        std::vector<double> qsum(R.ntuples);
+        x.d2h(qsum.data(), E->d_qsum.p, qsum.size() * 8);
+        x.sync();
+        long long ncand = 1;
+        for (int d = 0; d < D; ++d) ncand *= (long long)given[d].size();
+        auto* r = static_cast<cg_route_grid_result*>(std::calloc(1, sizeof(cg_route_grid_result)));
+        r->stages = C;
+        r->num_candidates = ncand;
+        std::vector<double> thr((size_t)ncand * D), ratios((size_t)ncand * C), q(ncand);
+        std::vector<cg_workload> wl((size_t)ncand * C);
+        for (long long c = 0; c < ncand; ++c) {
+            long long rem = c, tuple = 0, ts = 1;
+            std::vector<int> gi(D);
+            for (int d = D - 1; d >= 0; --d) {
+                gi[d] = (int)(rem % (long long)given[d].size());
+                rem /= (long long)given[d].size();
+            }
+            for (int d = 0; d < D; ++d) {
+                thr[(size_t)c * D + d] = given[d][gi[d]];
+                tuple += (long long)g2d[d][gi[d]] * ts;
+                ts *= R.G[d];
+            }
+            for (int i = 0; i < C; ++i) {
+                const long long w = R.off[i] + (i == 0 ? 0 : tuple % R.P[i]);
+                ratios[(size_t)c * C + i] = static_cast<double>(R.count[w]) / static_cast<double>(t.n);
+                const double* s = &R.stats[(size_t)w * 5];
+                wl[(size_t)c * C + i] = {s[0], s[1], s[2], s[3], s[4]};
+            }
+            q[c] = qsum[tuple] / static_cast<double>(t.n);
+        }
+        r->thresholds = hcopy(thr);
+        r->ratios = hcopy(ratios);
+        r->workloads = hcopy(wl);
+        r->quality = hcopy(q);
+        x.st.candidates = ncand;
+        x.st.distinct_candidates = R.ntuples;
+        x.st.gpu_launches = x.launches;
+        x.st.ms_total = timer.ms();
+        r->stats = x.st;
+        *out = r;
+    });
+}
+
+void cg_route_grid_result_free(cg_route_grid_result* r) {
+    if (!r) return;
+    std::free(r->thresholds);
+    std::free(r->ratios);
+    std::free(r->workloads);
+    std::free(r->quality);
+    std::free(r);
 }
 
 cg_status cg_stage_row(cg_engine* E, const cg_model* model, const cg_workload* w, const cg_hardware* hw,

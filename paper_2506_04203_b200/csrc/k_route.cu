@@ -34,58 +34,228 @@ namespace cg {
 
 namespace {
 
-__device__ __forceinline__ int rank_of(const double* __restrict__ v, int g, double s) {
-    // #{v <= s}: upper_bound with predicate (v <= s); NaN scores rank 0.
-    int lo = 0, hi = g;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (v[mid] <= s) lo = mid + 1;
-        else hi = mid;
+// #{v <= s} over the sorted distinct values v[0..g): upper_bound with the
+// predicate (v <= s), NaN scores rank 0.  Branch-free: the step sequence
+// depends only on g (warp-uniform), so lanes never diverge.
+__device__ __forceinline__ int rank_of(const double* __restrict__ v, int g, int top, double s) {
+    int pos = 0;
+    for (int b = top; b > 0; b >>= 1) {
+        const int q = pos + b;
+        pos = (q <= g && v[q - 1] <= s) ? q : pos;
     }
-    return lo;
+    return pos;
 }
 
 __device__ __forceinline__ bool token_ok(double x) {
     return x >= 0.0 && x < 4294967296.0 && x == trunc(x);
 }
 
-template <int D>
+// Warp-aggregated histogram update of NQ u64 words per cell: lanes with the
+// same cell are merged with __match_any_sync; each group's token sums are
+// reduced with two 16-bit-split __reduce_add_sync (exact for u32 tokens) and
+// its leader issues one atomic per word.  Words: [count?] then the sums.
+template <int NQ, bool COUNT>
+__device__ __forceinline__ void hist_add(unsigned long long* __restrict__ h, bool valid, unsigned cell,
+                                         const unsigned* v /*[NQ - COUNT]*/) {
+    constexpr int NV = NQ - (COUNT ? 1 : 0);
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(act, cell);
+    unsigned long long* p = h + (unsigned long long)cell * NQ;
+    if (__all_sync(act, peers == (1u << lane))) {
+        if (COUNT) atomicAdd(&p[0], 1ull);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) atomicAdd(&p[q + (COUNT ? 1 : 0)], (unsigned long long)v[q]);
+        return;
+    }
+    unsigned long long sums[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const unsigned lo = __reduce_add_sync(peers, v[q] & 0xffffu);
+        const unsigned hi = __reduce_add_sync(peers, v[q] >> 16);
+        sums[q] = ((unsigned long long)hi << 16) + lo;
+    }
+    if (lane == __ffs(peers) - 1) {
+        if (COUNT) atomicAdd(&p[0], (unsigned long long)__popc(peers));
+#pragma unroll
+        for (int q = 0; q < NV; ++q) atomicAdd(&p[q + (COUNT ? 1 : 0)], sums[q]);
+    }
+}
+
+__device__ __forceinline__ unsigned tok32(double x, bool& bad) {
+    const bool ok = token_ok(x);
+    bad |= !ok;
+    return ok ? (unsigned)x : 0u;
+}
+
+// K1: one streaming pass over the trace.  Each thread routes two consecutive
+// requests per iteration with 128-bit loads of every SoA column (scores of
+// the C-1 threshold stages, input tokens, C output-token columns) and writes
+// the packed ranks with one 128-bit store.  Aggregation (block-private in
+// shared memory when it fits, PRIV, else global): full rank cells carry
+// (count, sum_in, sum_out_{C-1}); the stage-i output sums (i < C-1) only
+// depend on dims < i and go to small marginal histograms over those dims.
+template <int D, bool PRIV>
 __global__ void __launch_bounds__(256) k_route_aggregate(RouteArgs a) {
-    extern __shared__ double s_grid[];
+    constexpr int C = D + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* sh_hist = reinterpret_cast<unsigned long long*>(smem_raw);
+    double* s_grid = reinterpret_cast<double*>(smem_raw + (PRIV ? (size_t)a.priv_words * 8 : 0));
     const double* gv = a.gvals;
     if (a.grid_in_smem) {
         for (int i = threadIdx.x; i < a.gtotal; i += blockDim.x) s_grid[i] = a.gvals[i];
-        __syncthreads();
         gv = s_grid;
     }
-    const int C = D + 1;
-    const int Q = 2 + C;
+    if (PRIV)
+        for (long long i = threadIdx.x; i < a.priv_words; i += blockDim.x) sh_hist[i] = 0ull;
+    __syncthreads();
+    unsigned long long* full = PRIV ? sh_hist : a.acc;
     bool bad = false;
-    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.n;
-         r += (long long)gridDim.x * blockDim.x) {
-        unsigned long long packed = 0;
-        long long cell = 0;
+    const long long n = a.n;
+    const long long npairs = (n + 1) >> 1;
+    const bool vec = (n & 1) == 0 && ((reinterpret_cast<unsigned long long>(a.scores) |
+                                        reinterpret_cast<unsigned long long>(a.in) |
+                                        reinterpret_cast<unsigned long long>(a.out) |
+                                        reinterpret_cast<unsigned long long>(a.ranks)) & 15ull) == 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // uniform trip count so every lane reaches the warp collectives
+    const long long first = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long iters = (npairs + stride - 1) / stride;
+    // software pipeline: the loads of iteration it+1 are in flight while
+    // iteration it is ranked and aggregated
+    double nsc[D > 0 ? D : 1][2], nxin[2], nxo[C][2];
+    auto load_pair = [&](long long r0, double (&sc)[D > 0 ? D : 1][2], double (&xin)[2], double (&xo)[C][2]) {
+        const bool v1 = r0 + 1 < n;
+        if (v1 && vec) {
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-            const double s = __ldg(&a.scores[(long long)d * a.n + r]);
-            const int rk = rank_of(gv + a.goff[d], a.G[d], s);
-            packed |= (unsigned long long)rk << (16 * d);
-            cell += (long long)rk * a.stride[d];
+            for (int d = 0; d < D; ++d) {
+                const double2 t = __ldcs(reinterpret_cast<const double2*>(a.scores + (long long)d * n + r0));
+                sc[d][0] = t.x;
+                sc[d][1] = t.y;
+            }
+            const double2 ti = __ldcs(reinterpret_cast<const double2*>(a.in + r0));
+            xin[0] = ti.x;
+            xin[1] = ti.y;
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const double2 t = __ldcs(reinterpret_cast<const double2*>(a.out + (long long)i * n + r0));
+                xo[i][0] = t.x;
+                xo[i][1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long r = r0 + e;
+                const bool ve = r < n;
+#pragma unroll
+                for (int d = 0; d < D; ++d) sc[d][e] = ve ? a.scores[(long long)d * n + r] : 0.0;
+                xin[e] = ve ? a.in[r] : 0.0;
+#pragma unroll
+                for (int i = 0; i < C; ++i) xo[i][e] = ve ? a.out[(long long)i * n + r] : 0.0;
+            }
         }
-        a.ranks[r] = packed;
-        const double xin = __ldg(&a.in[r]);
-        bad |= !token_ok(xin);
-        unsigned long long* h = a.hist + cell * Q;
-        atomicAdd(&h[0], 1ull);
-        atomicAdd(&h[1], (unsigned long long)(xin >= 0.0 && xin < 4294967296.0 ? xin : 0.0));
+    };
+    if (iters > 0) load_pair(2 * first, nsc, nxin, nxo);
+    for (long long it = 0; it < iters; ++it) {
+        const long long p = first + it * stride;
+        const long long r0 = 2 * p;
+        const bool v0 = r0 < n, v1 = r0 + 1 < n;
+        double sc[D > 0 ? D : 1][2], xin[2], xo[C][2];
 #pragma unroll
-        for (int i = 0; i < C; ++i) {
-            const double xo = __ldg(&a.out[(long long)i * a.n + r]);
-            bad |= !token_ok(xo);
-            atomicAdd(&h[2 + i], (unsigned long long)(xo >= 0.0 && xo < 4294967296.0 ? xo : 0.0));
+        for (int e = 0; e < 2; ++e) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) sc[d][e] = nsc[d][e];
+            xin[e] = nxin[e];
+#pragma unroll
+            for (int i = 0; i < C; ++i) xo[i][e] = nxo[i][e];
+        }
+        if (it + 1 < iters) load_pair(r0 + 2 * stride, nsc, nxin, nxo);
+        unsigned long long pk[2] = {0ull, 0ull};
+        unsigned cell[2] = {0u, 0u};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int rk = rank_of(gv + a.goff[d], a.G[d], a.gtop[d], sc[d][e]);
+                pk[e] |= (unsigned long long)rk << (16 * d);
+                cell[e] += (unsigned)rk * (unsigned)a.stride[d];
+            }
+        }
+        if (v1 && vec) {
+            *reinterpret_cast<ulonglong2*>(a.ranks + r0) = make_ulonglong2(pk[0], pk[1]);
+        } else {
+            if (v0) a.ranks[r0] = pk[0];
+            if (v1) a.ranks[r0 + 1] = pk[1];
+        }
+        // per-lane shared-memory atomics (hardware-serialised only on real
+        // address conflicts); the one-bin stage-0 marginal is a warp REDUX
+        unsigned s0lo = 0, s0hi = 0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const bool ve = e == 0 ? v0 : v1;
+            if (ve) {
+                unsigned long long* pf = full + (unsigned long long)cell[e] * 3;
+                atomicAdd(&pf[0], 1ull);
+                atomicAdd(&pf[1], (unsigned long long)tok32(xin[e], bad));
+                atomicAdd(&pf[2], (unsigned long long)tok32(xo[C - 1][e], bad));
+            }
+            if (C > 1) {
+                const unsigned v0t = ve ? tok32(xo[0][e], bad) : 0u;
+                s0lo += v0t & 0xffffu;
+                s0hi += v0t >> 16;
+            }
+#pragma unroll
+            for (int i = 1; i < C - 1; ++i) {
+                if (ve) {
+                    const unsigned mcell = cell[e] % (unsigned)a.stride[i];
+                    atomicAdd(full + a.marg_off[i] + mcell, (unsigned long long)tok32(xo[i][e], bad));
+                }
+            }
+        }
+        if (C > 1) {
+            const unsigned lo = __reduce_add_sync(0xffffffffu, s0lo);
+            const unsigned hi = __reduce_add_sync(0xffffffffu, s0hi);
+            if ((threadIdx.x & 31) == 0)
+                atomicAdd(full + a.marg_off[0], ((unsigned long long)hi << 16) + (unsigned long long)lo);
         }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, 1u);
+    if (PRIV) {
+        __syncthreads();
+        unsigned long long* part = a.partials + (long long)blockIdx.x * a.priv_words;
+        for (long long i = threadIdx.x; i < a.priv_words; i += blockDim.x) part[i] = sh_hist[i];
+    }
+}
+
+// Sum the block-private partials (or take the global accumulator) and expand
+// into the [cells][2+C] layout the dominance scan expects: the marginal sums
+// of stage i (i < C-1) sit at the cells whose dims >= i are at their maximum
+// rank, so the dominance prefix sum reproduces them at every stage-i query.
+__global__ void k_hist_expand(RouteArgs a, int C, int nblocks) {
+    const long long cell = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (cell >= a.cells) return;
+    const int Q = 2 + C;
+    auto acc = [&](long long w) -> unsigned long long {
+        if (nblocks == 0) return a.acc[w];
+        unsigned long long s = 0;
+        for (int b = 0; b < nblocks; ++b) s += a.partials[(long long)b * a.priv_words + w];
+        return s;
+    };
+    unsigned long long* h = a.hist + cell * Q;
+    h[0] = acc(cell * 3 + 0);
+    h[1] = acc(cell * 3 + 1);
+    h[2 + (C - 1)] = acc(cell * 3 + 2);
+    for (int i = 0; i < C - 1; ++i) {
+        bool at_max = true;
+        long long rem = cell;
+        for (int d = 0; d < C - 1; ++d) {
+            const long long coord = rem % (a.G[d] + 1);
+            rem /= (a.G[d] + 1);
+            if (d >= i && coord != a.G[d]) at_max = false;
+        }
+        h[2 + i] = at_max ? acc(a.marg_off[i] + (i == 0 ? 0 : cell % a.stride[i])) : 0ull;
+    }
 }
 
 // Inclusive prefix sums along dimension d of the (G_d+1)-extent histogram.
@@ -295,22 +465,48 @@ __global__ void __launch_bounds__(QT_THREADS) k_quality(const double* __restrict
 
 }  // namespace
 
-void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches) {
-    long long blocks = (a.n + 255) / 256;
-    long long cap = (long long)sm_count * 8;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    size_t smem = a.grid_in_smem ? (size_t)a.gtotal * sizeof(double) : 0;
-    switch (D) {
-        case 0: k_route_aggregate<0><<<(unsigned)blocks, 256, smem, s>>>(a); break;
-        case 1: k_route_aggregate<1><<<(unsigned)blocks, 256, smem, s>>>(a); break;
-        case 2: k_route_aggregate<2><<<(unsigned)blocks, 256, smem, s>>>(a); break;
-        case 3: k_route_aggregate<3><<<(unsigned)blocks, 256, smem, s>>>(a); break;
-        case 4: k_route_aggregate<4><<<(unsigned)blocks, 256, smem, s>>>(a); break;
-        default: throw EngineError(101, "GPU engine supports up to 5 cascade stages");
+template <int D>
+void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches) {
+    const size_t grid_smem = a.grid_in_smem ? (size_t)a.gtotal * sizeof(double) : 0;
+    const size_t hist_smem = (size_t)a.priv_words * 8;
+    const bool priv = a.partials != nullptr && hist_smem + grid_smem <= 96 * 1024;
+    const long long npairs = (a.n + 1) / 2;
+    long long blocks = (npairs + 255) / 256;
+    int nb = 0;
+    if (priv) {
+        auto kern = k_route_aggregate<D, true>;
+        const size_t smem = hist_smem + grid_smem;
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+        const long long cap = (long long)sm_count * (per_sm < 1 ? 1 : per_sm);
+        if (blocks > cap) blocks = cap;
+        if (blocks > a.max_partials) blocks = a.max_partials;
+        if (blocks < 1) blocks = 1;
+        kern<<<(unsigned)blocks, 256, smem, s>>>(a);
+        nb = (int)blocks;
+    } else {
+        CG_CUDA(cudaMemsetAsync(a.acc, 0, (size_t)a.priv_words * 8, s));
+        const long long cap = (long long)sm_count * 8;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        k_route_aggregate<D, false><<<(unsigned)blocks, 256, grid_smem, s>>>(a);
     }
     CG_LAUNCH_CHECK();
-    if (launches) ++*launches;
+    k_hist_expand<<<(unsigned)((a.cells + 255) / 256), 256, 0, s>>>(a, D + 1, nb);
+    CG_LAUNCH_CHECK();
+    if (launches) *launches += 2;
+}
+
+void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches) {
+    switch (D) {
+        case 0: launch_k1<0>(a, sm_count, s, launches); break;
+        case 1: launch_k1<1>(a, sm_count, s, launches); break;
+        case 2: launch_k1<2>(a, sm_count, s, launches); break;
+        case 3: launch_k1<3>(a, sm_count, s, launches); break;
+        case 4: launch_k1<4>(a, sm_count, s, launches); break;
+        default: throw EngineError(101, "GPU engine supports up to 5 cascade stages");
+    }
 }
 
 void launch_hist_scan(unsigned long long* hist, long long cells, int Q, const long long* stride,

@@ -127,6 +127,12 @@ class RouteResultC(ctypes.Structure):
                 ("stage_workloads", Workload * 8), ("quality", ctypes.c_double)]
 
 
+class RouteGridResultC(ctypes.Structure):
+    _fields_ = [("stages", ctypes.c_int32), ("num_candidates", ctypes.c_int64), ("thresholds", _DP),
+                ("ratios", _DP), ("workloads", ctypes.POINTER(Workload)), ("quality", _DP),
+                ("stats", SweepStats)]
+
+
 class RowResultC(ctypes.Structure):
     _fields_ = [("max_budget", ctypes.c_int32), ("latency", _DP),
                 ("plan_index", ctypes.POINTER(ctypes.c_int64)), ("num_plans", ctypes.c_int64),
@@ -139,7 +145,7 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, 
 
 EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_engine_set_collective", "cg_engine_set_option",
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
-            "cg_solve_min_max", "cg_generate_trace", "cg_version"]
+            "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free"]
 
 _lib = None
 
@@ -169,6 +175,11 @@ def library():
         L.cg_route.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), _DP, ctypes.POINTER(ctypes.c_int32),
                                ctypes.POINTER(RouteResultC), ctypes.POINTER(ctypes.c_int32)]
         L.cg_route.restype = Status
+        L.cg_route_grid.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), ctypes.POINTER(SweepConfigC),
+                                    ctypes.POINTER(ctypes.POINTER(RouteGridResultC))]
+        L.cg_route_grid.restype = Status
+        L.cg_route_grid_result_free.argtypes = [ctypes.POINTER(RouteGridResultC)]
+        L.cg_route_grid_result_free.restype = None
         L.cg_stage_row.argtypes = [ctypes.c_void_p, ctypes.POINTER(Model), ctypes.POINTER(Workload),
                                    ctypes.POINTER(Hardware), ctypes.POINTER(CostParams), ctypes.c_int32,
                                    ctypes.POINTER(ctypes.POINTER(RowResultC))]
@@ -414,6 +425,30 @@ class Engine:
         if with_accept:
             res["per_request_accept_stage"] = list(acc)
         return res
+
+    # -- batched route_trace over a threshold grid (the sweep's routing phase)
+    def route_grid(self, trace, cfg: Optional[dict] = None) -> list:
+        tb = _as_trace(trace)
+        tc = tb.c()
+        cc, keep2 = _sweep_config_c(cfg)
+        out = ctypes.POINTER(RouteGridResultC)()
+        _check(self._lib.cg_route_grid(self._h, ctypes.byref(tc), ctypes.byref(cc), ctypes.byref(out)))
+        try:
+            r = out.contents
+            self.last_stats = _stats_dict(r.stats)
+            C, K, D = r.stages, r.num_candidates, r.stages - 1
+            keys = ["arrival_rate", "mean_input_tokens", "mean_output_tokens", "p95_input_tokens",
+                    "p95_output_tokens"]
+            res = []
+            for c in range(K):
+                res.append({"thresholds": [r.thresholds[c * D + d] for d in range(D)],
+                            "ratios": [r.ratios[c * C + i] for i in range(C)],
+                            "stage_workloads": [{k: getattr(r.workloads[c * C + i], k) for k in keys}
+                                                for i in range(C)],
+                            "quality": r.quality[c]})
+            return res
+        finally:
+            self._lib.cg_route_grid_result_free(out)
 
     # -- cascade::costmodel::StageEvaluator::row
     def row(self, hw: dict, params: Optional[dict], model: dict, workload: dict, max_budget: int) -> dict:

@@ -1,11 +1,12 @@
-"""Routing/aggregation pass (K1) on a large trace, for the HBM roofline:
-one cg_route over the C5 trace (10M requests, 4 stages) and the C3 trace."""
-import os, sys, time
+"""Routing phase (K1-K3 + K2) over a large trace for the HBM roofline:
+cg_route_grid with the default decile grid over the C3 / C5 traces."""
+import os, sys, time, json
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 from paper_2506_04203_b200 import engine as eng, workloads as W
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 parts = [eng.generate_trace(s, seed) for s, seed in W.trace_specs(name)]
 t = eng.concat_traces(parts) if len(parts) > 1 else parts[0]
 C = t["scores"].shape[0]
@@ -14,6 +15,11 @@ import torch
 dev = {k: torch.from_numpy(np.ascontiguousarray(t[k])).cuda() for k in t}
 tb = eng.TraceBuffers(dev["arrival_s"].data_ptr(), dev["input_tokens"].data_ptr(), dev["output_tokens"].data_ptr(),
                       dev["scores"].data_ptr(), on_device=True, keep={"n": t["arrival_s"].shape[0], "stages": C, "t": dev})
-for rep in range(3):
-    r = E.route_trace(tb, [60.0] * (C - 1), [True] * C)
-print(name, "n", t["arrival_s"].shape[0], "C", C, "ratios", [round(x, 4) for x in r["ratios"]], flush=True)
+for rep in range(reps):
+    res = E.route_grid(tb, {})
+    st = E.last_stats
+    print(json.dumps({"config": name, "n": int(t["arrival_s"].shape[0]), "C": C, "candidates": len(res),
+                      "ms_k1": st["ms_k1"], "k1_bytes": st["k1_bytes"],
+                      "k1_GBps": st["k1_bytes"] / st["ms_k1"] / 1e6 if st["ms_k1"] else None,
+                      "ms_route": st["ms_route"], "ms_quality": st["ms_quality"], "ms_total": st["ms_total"]}),
+          flush=True)
