@@ -266,6 +266,16 @@ cg_status cg_stage_row(cg_engine* engine, const cg_model* model, const cg_worklo
                        int32_t max_budget, cg_row_result** out);
 void cg_row_result_free(cg_row_result* result);
 
+/* Host-only (no GPU): merge per-budget bests of `shards` disjoint plan-index
+ * shards of one row -- lat_bits/plan_index[s*(max_budget+1) + g], ~0 = none --
+ * with the same rule the multi-GPU device merge applies after its all-gather,
+ * then the reference's prefix minimum (costmodel.cpp:347-352, 398-412). */
+cg_status cg_merge_row_shards(const cg_model* model, const cg_hardware* hw, const cg_cost_params* params,
+                              int32_t max_budget, int32_t shards, const uint64_t* lat_bits,
+                              const uint64_t* plan_index, cg_row_result** out);
+/* Static contiguous split of `total` work items for `rank` of `world`. */
+void cg_shard_range(uint64_t total, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi);
+
 /* solve_min_max on a latency table entries[i*(gpu_budget+1) + f]
  * (INFINITY = masked cell).  Writes allocations[stages], per_stage[stages]
  * and *objective_L. */

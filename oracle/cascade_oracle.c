@@ -214,6 +214,8 @@ typedef struct {
     double* best_lat;   /* [N+1] */
     int* best_counts;   /* [(N+1)*MAXS] */
     char* has_best;
+    int64_t* best_idx;  /* [N+1] enumeration index of the best plan */
+    int64_t counter, lo, hi;  /* plan-index shard [lo, hi) */
 } rowctx;
 
 static int parts_less(const int* A, const int* B, int S) {
@@ -272,6 +274,8 @@ static double simulate(rowctx* x, int dp) {
 }
 
 static void visit_plan(rowctx* x, const int* counts, int used) {
+    const int64_t pidx = x->counter++;
+    if (pidx < x->lo || pidx >= x->hi) return;
     int ok = 1, dp = 0;
     double capacity = 0.0;
     for (int s = 0; s < x->S; ++s) {
@@ -290,6 +294,7 @@ static void visit_plan(rowctx* x, const int* counts, int used) {
         (lat == x->best_lat[used] && parts_less(counts, slot, x->S))) {
         x->has_best[used] = 1;
         x->best_lat[used] = lat;
+        if (x->best_idx) x->best_idx[used] = pidx;
         memcpy(slot, counts, sizeof(int) * MAXS);
     }
 }
@@ -311,8 +316,9 @@ static int workload_invalid(const double* w) {
     return w[0] < 0 || w[1] < 0 || w[2] < 0 || w[3] < 0 || w[4] < 0 || w[3] < w[1] || w[4] < w[2];
 }
 
-int co_row(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget, double* latency,
-           int* plan_counts, int* num_shapes, int* shapes) {
+static int co_row_impl(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
+                       double* latency, int* plan_counts, int* num_shapes, int* shapes, int64_t lo, int64_t hi,
+                       double* shard_lat, int64_t* shard_idx, int64_t* total_plans) {
     if (workload_invalid(w)) return E_INVALID;
     for (int f = 0; f <= max_budget; ++f) latency[f] = INFINITY;
     if (plan_counts) memset(plan_counts, 0, sizeof(int) * (size_t)(max_budget + 1) * MAXS);
@@ -369,9 +375,19 @@ int co_row(const co_model* m, const double* w, const co_hw* hw, const co_params*
     x.best_lat = (double*)malloc(sizeof(double) * (max_budget + 1));
     x.best_counts = (int*)calloc((size_t)(max_budget + 1) * MAXS, sizeof(int));
     x.has_best = (char*)calloc(max_budget + 1, 1);
+    x.best_idx = (int64_t*)malloc(sizeof(int64_t) * (max_budget + 1));
+    x.counter = 0;
+    x.lo = lo;
+    x.hi = hi;
     int counts[MAXS];
     memset(counts, 0, sizeof(counts));
     enum_rec(&x, 0, counts, 0);
+    if (total_plans) *total_plans = x.counter;
+    if (shard_lat)
+        for (int g = 0; g <= max_budget; ++g) {
+            shard_lat[g] = x.has_best[g] ? x.best_lat[g] : INFINITY;
+            shard_idx[g] = x.has_best[g] ? x.best_idx[g] : -1;
+        }
     /* prefix minimum, strict '<' (costmodel.cpp:398-412) */
     double running = INFINITY;
     int have = 0, run_g = 0;
@@ -397,7 +413,23 @@ int co_row(const co_model* m, const double* w, const co_hw* hw, const co_params*
     free(x.best_lat);
     free(x.best_counts);
     free(x.has_best);
+    free(x.best_idx);
     return OK;
+}
+
+int co_row(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget, double* latency,
+           int* plan_counts, int* num_shapes, int* shapes) {
+    return co_row_impl(m, w, hw, p, max_budget, latency, plan_counts, num_shapes, shapes, 0, INT64_MAX, NULL, NULL,
+                       NULL);
+}
+
+int co_row_shard(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
+                 int64_t plan_lo, int64_t plan_hi, double* best_lat, int64_t* best_idx, int64_t* total_plans) {
+    double* lat = (double*)malloc(sizeof(double) * (max_budget + 1));
+    int rc = co_row_impl(m, w, hw, p, max_budget, lat, NULL, NULL, NULL, plan_lo, plan_hi, best_lat, best_idx,
+                         total_plans);
+    free(lat);
+    return rc;
 }
 
 /* ---------------- inner min-max (innerplan.cpp:58-194) */

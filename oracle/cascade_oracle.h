@@ -37,6 +37,11 @@ int co_route(const double* arrival, const double* in_tok, const double* out_tok,
 int co_row(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
            double* latency, int* plan_counts, int* num_shapes, int* shapes);
 
+/* Per-budget best over the plan-index shard [plan_lo, plan_hi) of a row (no
+ * prefix minimum): best_lat[g] (INFINITY = none), best_idx[g] (-1 = none). */
+int co_row_shard(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
+                 int64_t plan_lo, int64_t plan_hi, double* best_lat, int64_t* best_idx, int64_t* total_plans);
+
 /* innerplan::solve_min_max on entries[i*(gpu_budget+1)+f].
  * All functions return -1 on success, else the cascade::Errc value. */
 int co_solve(const double* entries, int stages, int gpu_budget, int total_gpus, int* alloc, double* objective);

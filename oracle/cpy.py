@@ -155,6 +155,28 @@ def row(hw, params, model, workload, max_budget):
             "plan": [_plan_json(plans[f * MAXS:(f + 1) * MAXS].tolist(), sh) for f in range(max_budget + 1)]}
 
 
+def row_shard(hw, params, model, workload, max_budget, plan_lo, plan_hi):
+    """Per-budget best over plan indices [plan_lo, plan_hi): (lat_bits u64[N+1]
+    with ~0 = none, plan_index u64[N+1] with ~0 = none, total_plans)."""
+    w = np.array([workload[k] for k in ("arrival_rate", "mean_input_tokens", "mean_output_tokens",
+                                        "p95_input_tokens", "p95_output_tokens")], dtype=np.float64)
+    lat = np.zeros(max_budget + 1)
+    idx = np.zeros(max_budget + 1, dtype=np.int64)
+    total = ctypes.c_int64()
+    hwc, mc, pc = _hw(hw), _model(model), _params(params)
+    L = lib()
+    L.co_row_shard.restype = ctypes.c_int
+    rc = L.co_row_shard(ctypes.byref(mc), _P(w), ctypes.byref(hwc), ctypes.byref(pc), int(max_budget),
+                        ctypes.c_int64(plan_lo), ctypes.c_int64(plan_hi), _P(lat), _P(idx), ctypes.byref(total))
+    if rc != -1:
+        raise OracleError(rc)
+    bits = lat.view(np.uint64).copy()
+    bits[idx < 0] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    pidx = idx.astype(np.uint64)
+    pidx[idx < 0] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    return bits, pidx, total.value
+
+
 def solve(table, total_gpus):
     n = int(table["gpu_budget"])
     ent = np.array([[math.inf if v is None else v for v in r] for r in table["entries"]], dtype=np.float64)

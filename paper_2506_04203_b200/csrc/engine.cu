@@ -116,20 +116,10 @@ __global__ void k_merge_ranks(const unsigned long long* __restrict__ gathered, i
     const int row = (int)(c / (N + 1));
     const PlanSpace& sp = spaces[rows[row].space];
     unsigned long long bl = kInfBits, bp = ~0ull;
-    unsigned char A[kMaxShapes], B[kMaxShapes];
     for (int r = 0; r < world; ++r) {
         const unsigned long long l = gathered[(long long)r * 2 * cells + c];
         const unsigned long long p = gathered[(long long)r * 2 * cells + cells + c];
-        if (p == ~0ull) continue;
-        bool take = false;
-        if (bp == ~0ull || l < bl) {
-            take = true;
-        } else if (l == bl && p != bp) {
-            unrank_plan(sp, p, A);
-            unrank_plan(sp, bp, B);
-            take = parts_less(A, B, sp.S);
-        }
-        if (take) {
+        if (merge_take(sp, l, p, bl, bp)) {
             bl = l;
             bp = p;
         }
@@ -388,9 +378,9 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             prefix[i + 1] = prefix[i] + (P + item_plans - 1) / item_plans;
         }
         const unsigned long long total_items = prefix.back();
-        const unsigned long long lo = total_items * (unsigned long long)E.rank / (unsigned long long)E.world;
-        const unsigned long long hi =
-            total_items * (unsigned long long)(E.rank + 1) / (unsigned long long)E.world;
+        uint64_t lo64 = 0, hi64 = 0;
+        cg_shard_range(total_items, E.rank, E.world, &lo64, &hi64);
+        const unsigned long long lo = lo64, hi = hi64;
         int* rowids = E.d_rowids.as<int>(rl.size());
         unsigned long long* ipre = E.d_iprefix.as<unsigned long long>(prefix.size());
         x.h2d(rowids, rl.data(), rl.size() * sizeof(int));
@@ -1321,6 +1311,83 @@ void cg_route_grid_result_free(cg_route_grid_result* r) {
     std::free(r->workloads);
     std::free(r->quality);
     std::free(r);
+}
+
+// Host-side shard merge with the device merge's rule (merge_take): per budget
+// the best (latency, plan) over all shards, then the reference's prefix
+// minimum.  No GPU needed; used by the multi-rank CPU tests.
+cg_status cg_merge_row_shards(const cg_model* model, const cg_hardware* hw, const cg_cost_params* q,
+                              int32_t max_budget, int32_t shards, const uint64_t* lat_bits,
+                              const uint64_t* plan_index, cg_row_result** out) {
+    return guarded([&] {
+        if (out) *out = nullptr;
+        if (!model || !hw || !q || !lat_bits || !plan_index || !out || shards < 1 || max_budget < 0)
+            fail(CG_ERR_INVALID_INPUT, "invalid merge arguments");
+        const int N = max_budget;
+        HostPlanSpace hs;
+        hs.build(legal_shapes(*model, *hw, *q), N);
+        PlanSpace sp;
+        std::memset(&sp, 0, sizeof(sp));
+        sp.S = (int)hs.shapes.size();
+        sp.N = N;
+        for (int k = 0; k < sp.S; ++k) sp.shapes[k] = hs.shapes[k];
+        sp.ways = hs.ways.data();
+        sp.num_plans = hs.num_plans;
+        auto* r = static_cast<cg_row_result*>(std::calloc(1, sizeof(cg_row_result)));
+        r->max_budget = N;
+        r->latency = static_cast<double*>(std::malloc(sizeof(double) * (N + 1)));
+        r->plan_index = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (N + 1)));
+        std::vector<cg_plan> plans;
+        std::vector<cg_replica> reps;
+        std::map<unsigned long long, int64_t> ids;
+        double running = dinf();
+        unsigned long long run_plan = ~0ull;
+        r->latency[0] = dinf();
+        r->plan_index[0] = -1;
+        for (int g = 1; g <= N; ++g) {
+            unsigned long long bl = kInfBits, bp = ~0ull;
+            for (int s = 0; s < shards; ++s) {
+                const unsigned long long l = lat_bits[(size_t)s * (N + 1) + g];
+                const unsigned long long p = plan_index[(size_t)s * (N + 1) + g];
+                if (merge_take(sp, l, p, bl, bp)) {
+                    bl = l;
+                    bp = p;
+                }
+            }
+            if (bp != ~0ull) {
+                double l;
+                std::memcpy(&l, &bl, 8);
+                if (l < running) {
+                    running = l;
+                    run_plan = bp;
+                }
+            }
+            r->latency[g] = running;
+            r->plan_index[g] = -1;
+            if (run_plan != ~0ull) {
+                auto it = ids.find(run_plan);
+                if (it == ids.end()) {
+                    cg_plan cp;
+                    expand_plan(hs, (long long)run_plan, reps, cp);
+                    it = ids.emplace(run_plan, (int64_t)plans.size()).first;
+                    plans.push_back(cp);
+                }
+                r->plan_index[g] = it->second;
+            }
+        }
+        r->num_plans = (int64_t)plans.size();
+        r->plans = hcopy(plans);
+        r->num_replicas = (int64_t)reps.size();
+        r->replicas = hcopy(reps);
+        *out = r;
+    });
+}
+
+/* Item range [lo, hi) of `rank` among `world` for a list of `total` items (the
+ * static contiguous split used by every sharded kernel class). */
+void cg_shard_range(uint64_t total, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi) {
+    *lo = total * (uint64_t)rank / (uint64_t)world;
+    *hi = total * (uint64_t)(rank + 1) / (uint64_t)world;
 }
 
 cg_status cg_stage_row(cg_engine* E, const cg_model* model, const cg_workload* w, const cg_hardware* hw,

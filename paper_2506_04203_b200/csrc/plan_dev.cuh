@@ -10,12 +10,12 @@
 
 namespace cg {
 
-__device__ __forceinline__ unsigned long long ways_at(const PlanSpace& sp, int i, int b) {
+__host__ __device__ __forceinline__ unsigned long long ways_at(const PlanSpace& sp, int i, int b) {
     return sp.ways[(long long)i * (sp.N + 1) + b];
 }
 
 // plan index p (0-based) -> counts; returns the GPUs used
-__device__ inline int unrank_plan(const PlanSpace& sp, unsigned long long p, unsigned char* c) {
+__host__ __device__ inline int unrank_plan(const PlanSpace& sp, unsigned long long p, unsigned char* c) {
     unsigned long long q = p + 1;  // lexicographic rank including the empty multiset
     int b = sp.N;
     int used = 0;
@@ -37,7 +37,7 @@ __device__ inline int unrank_plan(const PlanSpace& sp, unsigned long long p, uns
 
 // successor in the recursion order (last shape fastest); false at the end.
 // `used` (GPUs) and `dp` (replicas) are maintained incrementally.
-__device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& used, int& dp) {
+__host__ __device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& used, int& dp) {
     for (int i = sp.S - 1; i >= 0; --i) {
         const int size = sp.shapes[i].gpus;
         if (used + size <= sp.N) {
@@ -53,9 +53,15 @@ __device__ inline bool next_plan(const PlanSpace& sp, unsigned char* c, int& use
     return false;
 }
 
+// Merge rule of per-budget bests across shards / ranks (the reference's
+// `better`, costmodel.cpp:347-352): smaller latency, then parts-lexicographic.
+// `ways` must point at the table the caller's memory space can read.
+__host__ __device__ inline bool merge_take(const PlanSpace& sp, unsigned long long lat, unsigned long long plan,
+                                           unsigned long long best_lat, unsigned long long best_plan);
+
 // '<' of CompactPlan::parts (vector<pair<shape, count>>, costmodel.cpp:351)
 // evaluated on dense count vectors.
-__device__ inline bool parts_less(const unsigned char* A, const unsigned char* B, int S) {
+__host__ __device__ inline bool parts_less(const unsigned char* A, const unsigned char* B, int S) {
     for (int s = 0; s < S; ++s) {
         if (A[s] == B[s]) continue;
         if (A[s] > 0 && B[s] > 0) return A[s] < B[s];
@@ -69,6 +75,17 @@ __device__ inline bool parts_less(const unsigned char* A, const unsigned char* B
         return false;
     }
     return false;
+}
+
+__host__ __device__ inline bool merge_take(const PlanSpace& sp, unsigned long long lat, unsigned long long plan,
+                                           unsigned long long best_lat, unsigned long long best_plan) {
+    if (plan == ~0ull) return false;
+    if (best_plan == ~0ull || lat < best_lat) return true;
+    if (lat != best_lat || plan == best_plan) return false;
+    unsigned char A[kMaxShapes], B[kMaxShapes];
+    unrank_plan(sp, plan, A);
+    unrank_plan(sp, best_plan, B);
+    return parts_less(A, B, sp.S);
 }
 
 }  // namespace cg

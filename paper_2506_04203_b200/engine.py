@@ -145,7 +145,8 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, 
 
 EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_engine_set_collective", "cg_engine_set_option",
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
-            "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free"]
+            "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
+            "cg_merge_row_shards", "cg_shard_range"]
 
 _lib = None
 
@@ -180,6 +181,13 @@ def library():
         L.cg_route_grid.restype = Status
         L.cg_route_grid_result_free.argtypes = [ctypes.POINTER(RouteGridResultC)]
         L.cg_route_grid_result_free.restype = None
+        L.cg_merge_row_shards.argtypes = [ctypes.POINTER(Model), ctypes.POINTER(Hardware), ctypes.POINTER(CostParams),
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.POINTER(RowResultC))]
+        L.cg_merge_row_shards.restype = Status
+        L.cg_shard_range.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+        L.cg_shard_range.restype = None
         L.cg_stage_row.argtypes = [ctypes.c_void_p, ctypes.POINTER(Model), ctypes.POINTER(Workload),
                                    ctypes.POINTER(Hardware), ctypes.POINTER(CostParams), ctypes.c_int32,
                                    ctypes.POINTER(ctypes.POINTER(RowResultC))]
@@ -503,6 +511,35 @@ def generate_trace(spec: dict, seed: int) -> dict:
                                max(n, 0), ctypes.byref(no), ctypes.byref(so)))
     return {"arrival_s": arr[:n], "input_tokens": inp[:n], "output_tokens": out[: n * c].reshape(c, n),
             "scores": sc[: n * c].reshape(c, n)}
+
+
+def shard_range(total: int, rank: int, world: int):
+    """Static contiguous split used by every sharded kernel class."""
+    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
+    library().cg_shard_range(int(total), int(rank), int(world), ctypes.byref(lo), ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def merge_row_shards(hw: dict, params: Optional[dict], model: dict, max_budget: int, lat_bits, plan_index) -> dict:
+    """Host-side merge of per-shard per-budget bests (no GPU), the rule the
+    multi-GPU path applies after its all-gather, then the prefix minimum."""
+    L = library()
+    lat = np.ascontiguousarray(lat_bits, dtype=np.uint64).reshape(-1)
+    idx = np.ascontiguousarray(plan_index, dtype=np.uint64).reshape(-1)
+    shards = lat.size // (max_budget + 1)
+    marr, keep = models_c([model])
+    hwc, pc = hardware_c(hw), params_c(params)
+    out = ctypes.POINTER(RowResultC)()
+    U64 = ctypes.POINTER(ctypes.c_uint64)
+    _check(L.cg_merge_row_shards(marr, ctypes.byref(hwc), ctypes.byref(pc), int(max_budget), int(shards),
+                                 lat.ctypes.data_as(U64), idx.ctypes.data_as(U64), ctypes.byref(out)))
+    try:
+        r = out.contents
+        lats = [r.latency[f] for f in range(r.max_budget + 1)]
+        return {"latency": [None if math.isinf(v) else v for v in lats],
+                "plan": [_plan_json(r, int(r.plan_index[f])) for f in range(r.max_budget + 1)]}
+    finally:
+        L.cg_row_result_free(out)
 
 
 def concat_traces(parts: Sequence[dict]) -> dict:

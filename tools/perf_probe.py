@@ -6,13 +6,14 @@ from paper_2506_04203_b200 import engine as eng, workloads as W
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 count = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-" else None
 prunes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1]
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 parts = [eng.generate_trace(s, seed) for s, seed in W.trace_specs(name, count)]
 t = eng.concat_traces(parts) if len(parts) > 1 else parts[0]
 cfg, N = W.planner_config(name, t["scores"])
 E = eng.Engine(0)
 for prune in prunes:
     E.set_option("prune", prune)
-    for rep in range(2):
+    for rep in range(reps):
         t0 = time.time()
         res = E.sweep(t, cfg["models"], cfg["hardware"], cfg["cost_model"], N, cfg["sweep"])
         dt = time.time() - t0
