@@ -99,16 +99,18 @@ enum : int { CTR_STABLE = 0, CTR_FULL = 1, CTR_PRUNED = 2, CTR_STEPS = 3, CTR_BO
              CTR_COUNT = 8 };
 enum : int { SIM_RANGE = 0, SIM_LIST = 1, SIM_DEEP = 2 };
 
+// Work items: (row << 44) | plan index.
+constexpr int kItemPlanBits = 44;
+constexpr unsigned long long kItemPlanMask = (1ull << kItemPlanBits) - 1ull;
+
 struct SimArgs {
-    int N, n_req, K, prune, item_plans;
-    int dp_lo, dp_hi;                          // SIM_RANGE: plans with dp in (dp_lo, dp_hi]
+    int N, n_req, K, prune;
     int kstar;                                 // index of the K-th largest CRN output
-    int nrows;                                 // rows of this class
-    const int* row_ids;                        // class rows -> global row index
-    const unsigned long long* item_prefix;     // [nrows+1] cumulative item counts
+    int check_stable;                          // 1: items are not pre-filtered (seeds)
+    int seeds;                                 // 1: count completions as seeding work
+    const unsigned long long* items;           // packed (row, plan) work items
     unsigned long long nitems;
     unsigned long long* item_counter;
-    const SimItem* deep_items;                 // DEEP: one plan per item
     const RowDesc* rows;
     const PlanSpace* spaces;
     RowTables tab;
@@ -117,12 +119,31 @@ struct SimArgs {
     TieEntry* ties;
     unsigned long long* tie_count;
     unsigned long long tie_cap;
-    SimItem* ovf;
+    unsigned long long* ovf;                   // packed items whose smem ring overflowed
     unsigned long long* ovf_count;
     unsigned long long ovf_cap;
     double* scratch;                           // [slots][n_req]
     double* ring_global;                       // DEEP: [warps][32*R*ring_cap]
     int ring_cap;
+    unsigned long long* counters;
+};
+
+struct FilterArgs {
+    int N, n_req, kstar, prune;
+    int nrows;                                 // rows with plans
+    const int* row_ids;
+    const unsigned long long* chunk_prefix;    // [nrows+1] cumulative chunk counts per row
+    unsigned long long chunk_base;             // first chunk of this launch (waves / rank shard)
+    unsigned long long nchunks;                // chunks in this launch
+    int chunk;                                 // plans per chunk
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    RowTables tab;
+    const unsigned long long* ub;
+    unsigned long long* lists[7];
+    unsigned long long* keys[7];               // coarse service-bound order keys
+    unsigned long long* list_count;            // [7]
+    unsigned long long list_cap;               // per class
     unsigned long long* counters;
 };
 
@@ -136,6 +157,7 @@ void class_shape(int cls, int* W, int* R);
 void class_dp_range(int cls, int* lo, int* hi);
 SimGeometry sim_geometry(int cls, int mode, int sm_count);
 void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches);
+void launch_plan_filter(const FilterArgs& a, cudaStream_t s, int* launches);
 void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out);
 

@@ -150,7 +150,7 @@ struct cg_engine {
     DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
     DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
-        d_scratch, d_ring, d_seeds, d_partials, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
+        d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc;
 };
@@ -265,7 +265,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     x.fill(ub, cells, kInfBits);
     TieEntry* ties = E.d_ties.as<TieEntry>(E.tie_cap);
     unsigned long long* tiecnt = E.d_tiecnt.as<unsigned long long>(1);
-    SimItem* ovf = E.d_ovf.as<SimItem>(E.ovf_cap);
+    unsigned long long* ovf = E.d_ovf.as<unsigned long long>(E.ovf_cap);
     unsigned long long* ovfcnt = E.d_ovfcnt.as<unsigned long long>(1);
     unsigned long long* ovfcnt2 = E.d_ovfcnt2.as<unsigned long long>(1);
     unsigned long long* ctrs = E.d_ctrs.as<unsigned long long>(CTR_COUNT);
@@ -283,27 +283,22 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
         kstar = idx[K - 1];
     }
-    // Every row is simulated by the kernels of each replica-count class its
-    // plans can fall in (lane width W matched to the plan's replica count).
-    std::map<int, std::vector<int>> by_cls;
+    // rows with a non-empty plan space
+    std::vector<int> prow;
+    std::vector<unsigned long long> chunk_prefix(1, 0);
+    const int chunk = 64;
     for (int r = 0; r < nrows; ++r) {
         const auto& sp = hs[rows[r].space];
         x.st.plans_enumerated += (long long)sp.num_plans;
         if (sp.num_plans == 0 || N < 1) continue;
-        const int dpmax = N / sp.min_gpus;
-        for (int cls = 0; cls < 7; ++cls) {
-            int lo, hi;
-            class_dp_range(cls, &lo, &hi);
-            if (lo < dpmax) by_cls[cls].push_back(r);
-        }
+        prow.push_back(r);
+        chunk_prefix.push_back(chunk_prefix.back() + (sp.num_plans + chunk - 1) / chunk);
     }
     long long max_slots = 1;
-    for (auto& kv : by_cls) {
-        SimGeometry g = sim_geometry(kv.first, SIM_RANGE, E.sm_count);
-        SimGeometry gd = sim_geometry(kv.first, SIM_DEEP, E.sm_count);
-        max_slots = std::max({max_slots, g.slots, gd.slots});
+    for (int cls = 0; cls < 7; ++cls) {
+        max_slots = std::max(max_slots, sim_geometry(cls, SIM_LIST, E.sm_count).slots);
+        max_slots = std::max(max_slots, sim_geometry(cls, SIM_DEEP, E.sm_count).slots);
     }
-    max_slots = std::max(max_slots, sim_geometry(3, SIM_LIST, E.sm_count).slots);
     double* scratch = E.d_scratch.as<double>((size_t)max_slots * n_req);
     int ring_cap = 1;
     while (ring_cap < n_req) ring_cap <<= 1;
@@ -330,88 +325,115 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     base.counters = ctrs;
     base.ring_cap = ring_cap;
 
+    // Runs one packed work list through the class kernel, then the deep-queue
+    // re-runs of its ring overflows.
+    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds) {
+        if (nitems == 0) return;
+        CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
+        CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
+        SimArgs a = base;
+        a.items = items;
+        a.nitems = nitems;
+        a.check_stable = seeds ? 1 : 0;
+        a.seeds = seeds ? 1 : 0;
+        launch_sim(a, cls, SIM_LIST, E.sm_count, x.s, &x.launches, nullptr);
+        unsigned long long novf = 0;
+        x.d2h(&novf, ovfcnt, 8);
+        x.sync();
+        if (novf > (unsigned long long)E.ovf_cap) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
+        if (!seeds) x.st.plans_overflow += (long long)novf;
+        if (novf > 0 && !seeds) {  // deep-queue re-runs (rings in global memory, capacity >= n_req)
+            SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
+            double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
+            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
+            CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
+            SimArgs d = a;
+            d.items = ovf;
+            d.nitems = novf;
+            d.ring_global = ring;
+            d.ovf_count = ovfcnt2;
+            launch_sim(d, cls, SIM_DEEP, E.sm_count, x.s, &x.launches, nullptr);
+        }
+    };
+
     CG_CUDA(cudaEventRecord(E.ev[8], x.s));
     // Bound seeding: homogeneous plans (c replicas of one shape) of the heavy
-    // rows first, so the exact pruning bound is tight from the start.  Seeds
-    // are re-visited by the range kernels (idempotent), so this only moves work.
+    // rows first, so the exact bounds are tight from the start.  Seeds are
+    // re-visited by the filtered lists (idempotent), so this only moves work.
     if (E.prune && E.world == 1) {
-        std::vector<SimItem> seeds;
+        std::vector<unsigned long long> seeds;
         for (int r = 0; r < nrows; ++r) {
             const auto& sp = hs[rows[r].space];
             if (sp.num_plans < 4096 || N < 1) continue;
             const int S = (int)sp.shapes.size();
             for (int sidx = 0; sidx < S; ++sidx)
                 for (int c = 1; c * sp.shapes[sidx].gpus <= N && c <= 32; ++c) {
-                    // rank of the count vector (c at sidx, zeros elsewhere)
-                    unsigned long long q = 0;
-                    int b = N;
-                    for (int k = 0; k < c; ++k) q += sp.w(sidx + 1, b - k * sp.shapes[sidx].gpus);
-                    seeds.push_back(SimItem{r, 0, q - 1, q});
+                    unsigned long long q = 0;  // lexicographic rank of (0..0, c, 0..0)
+                    for (int k = 0; k < c; ++k) q += sp.w(sidx + 1, N - k * sp.shapes[sidx].gpus);
+                    seeds.push_back(((unsigned long long)r << kItemPlanBits) | (q - 1));
                 }
         }
         if (!seeds.empty()) {
-            SimItem* dseeds = E.d_seeds.as<SimItem>(seeds.size());
-            x.h2d(dseeds, seeds.data(), seeds.size() * sizeof(SimItem));
-            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
-            CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
-            SimArgs a = base;
-            a.deep_items = dseeds;
-            a.nitems = seeds.size();
-            launch_sim(a, 3, SIM_LIST, E.sm_count, x.s, &x.launches, nullptr);
+            unsigned long long* dseeds = E.d_seeds.as<unsigned long long>(seeds.size());
+            x.h2d(dseeds, seeds.data(), seeds.size() * 8);
+            run_list(dseeds, seeds.size(), 3, true);
         }
     }
-    for (auto& kv : by_cls) {
-        const int cls = kv.first;
-        const auto& rl = kv.second;
-        // item size: large enough to amortise unranking, small enough that every
-        // group slot of the persistent grid gets >= ~16 items
-        unsigned long long class_plans = 0;
-        for (int r : rl) class_plans += hs[rows[r].space].num_plans;
-        const SimGeometry geo = sim_geometry(cls, SIM_RANGE, E.sm_count);
-        const unsigned long long per =
-            std::max<unsigned long long>(1ull, class_plans / ((unsigned long long)geo.slots * 16ull));
-        const int item_plans = (int)std::min<unsigned long long>((unsigned long long)E.item_plans,
-                                                                 std::max<unsigned long long>(4ull, per));
-        std::vector<unsigned long long> prefix(rl.size() + 1, 0);
-        for (size_t i = 0; i < rl.size(); ++i) {
-            const unsigned long long P = hs[rows[rl[i]].space].num_plans;
-            prefix[i + 1] = prefix[i] + (P + item_plans - 1) / item_plans;
-        }
-        const unsigned long long total_items = prefix.back();
-        uint64_t lo64 = 0, hi64 = 0;
-        cg_shard_range(total_items, E.rank, E.world, &lo64, &hi64);
-        const unsigned long long lo = lo64, hi = hi64;
-        int* rowids = E.d_rowids.as<int>(rl.size());
-        unsigned long long* ipre = E.d_iprefix.as<unsigned long long>(prefix.size());
-        x.h2d(rowids, rl.data(), rl.size() * sizeof(int));
-        x.h2d(ipre, prefix.data(), prefix.size() * sizeof(unsigned long long));
-        x.h2d(ictr, &lo, 8);
-        CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
-
-        SimArgs a = base;
-        a.item_plans = item_plans;
-        class_dp_range(cls, &a.dp_lo, &a.dp_hi);
-        a.nrows = (int)rl.size();
-        a.row_ids = rowids;
-        a.item_prefix = ipre;
-        a.nitems = hi;
-        if (hi > lo) launch_sim(a, cls, SIM_RANGE, E.sm_count, x.s, &x.launches, nullptr);
-        unsigned long long novf = 0;
-        x.d2h(&novf, ovfcnt, 8);
-        x.sync();
-        if (novf > (unsigned long long)E.ovf_cap) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
-        x.st.plans_overflow += (long long)novf;
-        if (novf > 0) {  // deep-queue re-runs (rings in global memory, capacity >= n_req)
-            SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
-            double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
-            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
-            CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
-            SimArgs d = a;
-            d.deep_items = ovf;
-            d.nitems = novf;
-            d.ring_global = ring;
-            d.ovf_count = ovfcnt2;
-            launch_sim(d, cls, SIM_DEEP, E.sm_count, x.s, &x.launches, nullptr);
+    // Filter waves: enumerate every plan once, keep stable + not-bounded plans
+    // in per-class lists, simulate each list with its lane width.
+    if (!prow.empty()) {
+        int* rowids = E.d_rowids.as<int>(prow.size());
+        unsigned long long* cpre = E.d_iprefix.as<unsigned long long>(chunk_prefix.size());
+        x.h2d(rowids, prow.data(), prow.size() * sizeof(int));
+        x.h2d(cpre, chunk_prefix.data(), chunk_prefix.size() * 8);
+        uint64_t c_lo = 0, c_hi = 0;
+        cg_shard_range(chunk_prefix.back(), E.rank, E.world, &c_lo, &c_hi);
+        const unsigned long long wave_chunks = (16ull << 20) / chunk;
+        const unsigned long long cap = wave_chunks * chunk;
+        unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
+        unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)7 * cap);
+        unsigned long long* tk = E.d_lk1.as<unsigned long long>(cap);
+        unsigned long long* tv = E.d_lv1.as<unsigned long long>(cap);
+        unsigned int* rsh = E.d_rshist.as<unsigned int>(radix_hist_entries((long long)cap));
+        unsigned long long* lcount = E.d_lcount.as<unsigned long long>(7);
+        for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
+            const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);
+            CG_CUDA(cudaMemsetAsync(lcount, 0, 7 * 8, x.s));
+            FilterArgs fa{};
+            fa.N = N;
+            fa.n_req = n_req;
+            fa.kstar = kstar;
+            fa.prune = E.prune;
+            fa.nrows = (int)prow.size();
+            fa.row_ids = rowids;
+            fa.chunk_prefix = cpre;
+            fa.chunk_base = w0;
+            fa.nchunks = nch;
+            fa.chunk = chunk;
+            fa.rows = base.rows;
+            fa.spaces = base.spaces;
+            fa.tab = tab;
+            fa.ub = ub;
+            for (int c = 0; c < 7; ++c) {
+                fa.lists[c] = lists + (size_t)c * cap;
+                fa.keys[c] = lkeys + (size_t)c * cap;
+            }
+            fa.list_count = lcount;
+            fa.list_cap = cap;
+            fa.counters = ctrs;
+            launch_plan_filter(fa, x.s, &x.launches);
+            unsigned long long counts[7];
+            x.d2h(counts, lcount, sizeof(counts));
+            x.sync();
+            for (int c = 6; c >= 0; --c) {
+                unsigned long long* items = lists + (size_t)c * cap;
+                if (E.prune && counts[c] > 1) {  // ascending service bound (16-bit key: 2 passes)
+                    const int par = radix_sort_u64(lkeys + (size_t)c * cap, items, tk, tv, (long long)counts[c],
+                                                   0xffffull, rsh, x.s, &x.launches);
+                    if (par) items = tv;
+                }
+                run_list(items, counts[c], c, false);
+            }
         }
     }
     CG_CUDA(cudaEventRecord(E.ev[9], x.s));

@@ -46,6 +46,10 @@ constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
 constexpr unsigned long long kEmpty = ~0ull;
 constexpr unsigned FULL = 0xffffffffu;
 
+__device__ __forceinline__ int class_of_dp(int dp) {
+    return dp <= 4 ? 0 : dp <= 8 ? 1 : dp <= 16 ? 2 : dp <= 32 ? 3 : dp <= 64 ? 4 : dp <= 128 ? 5 : 6;
+}
+
 // ---------------------------------------------------------------------------
 // Row setup
 
@@ -134,7 +138,7 @@ struct GroupShared {
 // MODE: 0 = plan-index ranges (smem rings), 1 = explicit plan list (smem
 // rings; bound seeding), 2 = explicit list with global-memory rings (deep
 // re-runs of ring overflows).
-enum : int { MODE_RANGE = 0, MODE_LIST = 1, MODE_DEEP = 2 };
+enum : int { MODE_LIST = 1, MODE_DEEP = 2 };
 
 template <int W, int R, int MODE>
 struct Traits {
@@ -152,101 +156,68 @@ __device__ __forceinline__ void count_add(unsigned long long* ctr, unsigned long
     if (v) atomicAdd(ctr, v);
 }
 
-// Leader lane: advance to the next plan of this kernel's dp class that is
-// stable (costmodel.cpp:366-376) and not excluded by the exact service-time
-// bound; or mark the group done.
+// Exact service-time lower bound of a plan's p95 (see the header comment of
+// k_plan_filter); `counts` over the row's shapes.
+__device__ __forceinline__ double service_bound(const SimArgs& a, int row, const PlanSpace& sp,
+                                                const unsigned char* counts) {
+    const long long rb = (long long)row * kMaxShapes;
+    const double o_k = a.tab.O[(long long)row * a.n_req + a.kstar];
+    const double t_max = a.tab.T[(long long)row * a.n_req + a.n_req - 1];
+    double lb = __longlong_as_double(0x7ff0000000000000ll);
+    for (int s = 0; s < sp.S; ++s) {
+        if (!counts[s]) continue;
+        const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
+        lb = v < lb ? v : lb;
+    }
+    return lb * (1.0 - 1e-12) - 1e-12 * t_max;
+}
+
+// Leader lane: pop the next (row, plan) work item of this kernel's list and
+// unrank it; items come from k_plan_filter (already stable, class-matched) or
+// are seeds / overflow re-runs.  The service-time bound is re-checked against
+// the live bound (it tightens while the kernel runs).
 template <int MODE>
 __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
     while (true) {
-        if (gs.has_item && gs.plan + 1 < gs.hi) {
-            const PlanSpace& sp = a.spaces[a.rows[gs.row].space];
-            int used = gs.used, dpe = gs.dp_enum;
-            next_plan(sp, gs.counts, used, dpe);
-            gs.used = used;
-            gs.dp_enum = dpe;
-            gs.plan += 1;
-        } else {
-            const unsigned long long it = atomicAdd(a.item_counter, 1ull);
-            if (it >= a.nitems) {
-                gs.status = ST_DONE;
-                gs.has_item = 0;
-                return;
-            }
-            int row;
-            unsigned long long lo, hi;
-            if (MODE != MODE_RANGE) {
-                const SimItem si = a.deep_items[it];
-                row = si.row;
-                lo = si.lo;
-                hi = si.hi;
-            } else {
-                int l = 0, h = a.nrows - 1;  // item_prefix[l] <= it < item_prefix[l+1]
-                while (l < h) {
-                    const int mid = (l + h + 1) >> 1;
-                    if (a.item_prefix[mid] <= it) l = mid;
-                    else h = mid - 1;
-                }
-                row = a.row_ids[l];
-                const unsigned long long j = it - a.item_prefix[l];
-                const unsigned long long P = a.spaces[a.rows[row].space].num_plans;
-                hi = P - j * (unsigned long long)a.item_plans;  // descending items
-                lo = hi > (unsigned long long)a.item_plans ? hi - a.item_plans : 0ull;
-            }
-            gs.row = row;
-            gs.plan = lo;
-            gs.hi = hi;
-            gs.has_item = 1;
-            const PlanSpace& sp = a.spaces[a.rows[row].space];
-            gs.used = unrank_plan(sp, lo, gs.counts);
-            int dpe = 0;
-            for (int s = 0; s < sp.S; ++s) dpe += gs.counts[s];
-            gs.dp_enum = dpe;
+        const unsigned long long it = atomicAdd(a.item_counter, 1ull);
+        if (it >= a.nitems) {
+            gs.status = ST_DONE;
+            return;
         }
-        // this kernel simulates only its replica-count class (lane width W)
-        if (MODE == MODE_RANGE && (gs.dp_enum <= a.dp_lo || gs.dp_enum > a.dp_hi)) continue;
-        const RowDesc& rd = a.rows[gs.row];
+        const unsigned long long item = a.items[it];
+        const int row = (int)(item >> kItemPlanBits);
+        const unsigned long long plan = item & kItemPlanMask;
+        const RowDesc& rd = a.rows[row];
         const PlanSpace& sp = a.spaces[rd.space];
-        const long long rb = (long long)gs.row * kMaxShapes;
-        const unsigned char* ok = a.tab.shape_ok + rb;
-        const double* ms = a.tab.mean_service + rb;
-        bool good = true;
-        double capacity = 0.0;
-        for (int s = 0; s < sp.S; ++s) {
-            const int c = gs.counts[s];
-            if (!c) continue;
-            if (!ok[s]) {
-                good = false;
-                break;
-            }
-            capacity = __dadd_rn(capacity, __ddiv_rn((double)c, ms[s]));
-        }
-        if (!good || rd.rate >= capacity) continue;
-        if (MODE == MODE_RANGE) atomicAdd(&a.counters[CTR_STABLE], 1ull);
-        if (a.prune && MODE != MODE_DEEP) {
-            // Exact bound without simulation: every sojourn on shape s is >=
-            // fl(fl(fl(t+p_s)+fl(o d_s))-t) >= (p_s+o d_s)(1-5u) - 2u t, and
-            // min_s(p_s + o d_s) is increasing in o, so the K-th largest sojourn
-            // is >= min_{s in plan}(p_s + o_(K) d_s)(1-1e-12) - 1e-12 T_max,
-            // o_(K) = the K-th largest CRN output (index kstar).  A plan whose
-            // bound exceeds the best latency already found at <= its budget can
-            // never enter the row.
-            const double o_k = a.tab.O[(long long)gs.row * a.n_req + a.kstar];
-            const double t_max = a.tab.T[(long long)gs.row * a.n_req + a.n_req - 1];
-            double lb = __longlong_as_double(0x7ff0000000000000ll);
+        gs.used = unrank_plan(sp, plan, gs.counts);
+        int dp = 0;
+        for (int s = 0; s < sp.S; ++s) dp += gs.counts[s];
+        if (a.check_stable) {  // seeds are not pre-filtered
+            const long long rb = (long long)row * kMaxShapes;
+            bool good = true;
+            double capacity = 0.0;
             for (int s = 0; s < sp.S; ++s) {
-                if (!gs.counts[s]) continue;
-                const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
-                lb = v < lb ? v : lb;
+                const int c = gs.counts[s];
+                if (!c) continue;
+                if (!a.tab.shape_ok[rb + s]) {
+                    good = false;
+                    break;
+                }
+                capacity = __dadd_rn(capacity, __ddiv_rn((double)c, a.tab.mean_service[rb + s]));
             }
-            lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
+            if (!good || rd.rate >= capacity) continue;
+        }
+        if (a.prune && MODE != MODE_DEEP && !a.check_stable) {
             const double U = __longlong_as_double(
-                (long long)*(volatile unsigned long long*)&a.ub[(long long)gs.row * (a.N + 1) + gs.used]);
-            if (lb > U) {
+                (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gs.used]);
+            if (service_bound(a, row, sp, gs.counts) > U) {
                 atomicAdd(&a.counters[CTR_BOUND], 1ull);
                 continue;
             }
         }
-        gs.dp = gs.dp_enum;
+        gs.row = row;
+        gs.plan = plan;
+        gs.dp = dp;
         gs.status = ST_RUN;
         return;
     }
@@ -359,10 +330,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
     const int ring_mask = DEEP ? a.ring_cap - 1 : CAP - 1;
     const int ring_cap = DEEP ? a.ring_cap : CAP;
 
-    if (gl == 0) {
-        gs.status = ST_NEED;
-        gs.has_item = 0;
-    }
+    if (gl == 0) gs.status = ST_NEED;
     __syncwarp();
 
     int status = ST_NEED;
@@ -513,7 +481,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                 if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
-                        if (idx < a.ovf_cap) a.ovf[idx] = SimItem{row, 0, plan, plan + 1};
+                        if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
                     }
                     steps += k;
                     status = ST_NEED;
@@ -543,7 +511,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                 if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
-                        if (idx < a.ovf_cap) a.ovf[idx] = SimItem{row, 0, plan, plan + 1};
+                        if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
                     }
                 } else if (a.prune && tot >= a.K) {
                     pruned += 1;
@@ -575,8 +543,8 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
     // per-lane counters -> global (leaders only to avoid double counting)
     if (gl == 0) {
         count_add(&a.counters[CTR_STEPS], steps);
-        count_add(&a.counters[MODE == MODE_LIST ? CTR_SEED : CTR_FULL], full);
-        count_add(&a.counters[MODE == MODE_LIST ? CTR_SEED : CTR_PRUNED], pruned);
+        count_add(&a.counters[a.seeds ? CTR_SEED : CTR_FULL], full);
+        count_add(&a.counters[a.seeds ? CTR_SEED : CTR_PRUNED], pruned);
     }
 }
 
@@ -629,6 +597,108 @@ __global__ void k_row_prefix(ResolveArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Plan filter: every plan of every row is enumerated exactly once, by a thread
+// per chunk of consecutive plan indices (unrank the first, lexicographic
+// successor for the rest).  A plan survives if it is stable
+// (costmodel.cpp:366-376) and its exact service-time bound does not exceed the
+// best latency already known at <= its budget: every sojourn on shape s is >=
+// fl(fl(fl(t+p_s)+fl(o d_s))-t) >= (p_s+o d_s)(1-5u) - 2u t (u = 2^-53), and
+// min_s(p_s + o d_s) is increasing in o, so the K-th largest sojourn is >=
+// min_{s in plan}(p_s + o_(K) d_s)(1-1e-12) - 1e-12 T_max where o_(K) is the
+// K-th largest CRN output.  Survivors go to the work list of their
+// replica-count class (warp-aggregated appends).
+__global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
+    const unsigned long long chunk = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    const bool active = chunk < a.nchunks;
+    int row = 0;
+    unsigned long long lo = 0, hi = 0;
+    if (active) {
+        int l = 0, h = a.nrows - 1;  // chunk_prefix[l] <= chunk < chunk_prefix[l+1]
+        while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (a.chunk_prefix[mid] <= chunk + a.chunk_base) l = mid;
+            else h = mid - 1;
+        }
+        row = a.row_ids[l];
+        // reversed within the row: large-shape plans (best bounds) first
+        const unsigned long long nrc = a.chunk_prefix[l + 1] - a.chunk_prefix[l];
+        const unsigned long long j = nrc - 1 - (chunk + a.chunk_base - a.chunk_prefix[l]);
+        const unsigned long long P = a.spaces[a.rows[row].space].num_plans;
+        lo = j * (unsigned long long)a.chunk;
+        hi = lo + a.chunk < P ? lo + a.chunk : P;
+    }
+    const RowDesc rd = a.rows[active ? row : 0];
+    const PlanSpace& sp = a.spaces[rd.space];
+    const long long rb = (long long)row * kMaxShapes;
+    unsigned char c[kMaxShapes];
+    int used = 0, dp = 0;
+    if (active) {
+        used = unrank_plan(sp, lo, c);
+        for (int s = 0; s < sp.S; ++s) dp += c[s];
+    }
+    const double o_k = active ? a.tab.O[(long long)row * a.n_req + a.kstar] : 0.0;
+    const double t_max = active ? a.tab.T[(long long)row * a.n_req + a.n_req - 1] : 0.0;
+    unsigned long long stable = 0, skipped = 0;
+    const unsigned long long trips = a.chunk;
+    for (unsigned long long k = 0; k < trips; ++k) {
+        const unsigned long long p = lo + k;
+        const bool live = active && p < hi;
+        if (live && k > 0) next_plan(sp, c, used, dp);
+        int cls = -1;
+        unsigned long long key = 0;
+        if (live) {
+            bool good = true;
+            double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll);
+            for (int s = 0; s < sp.S; ++s) {
+                const int cnt = c[s];
+                if (!cnt) continue;
+                if (!a.tab.shape_ok[rb + s]) {
+                    good = false;
+                    break;
+                }
+                capacity = __dadd_rn(capacity, __ddiv_rn((double)cnt, a.tab.mean_service[rb + s]));
+                const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
+                lb = v < lb ? v : lb;
+            }
+            if (good && rd.rate < capacity) {
+                ++stable;
+                bool keep = true;
+                lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
+                key = dbl_to_key(lb) >> 48;  // coarse order key: likely-good plans first
+                if (a.prune) {
+                    const double U = __longlong_as_double(
+                        (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
+                    if (lb > U) {
+                        keep = false;
+                        ++skipped;
+                    }
+                }
+                if (keep) cls = class_of_dp(dp);
+            }
+        }
+        // warp-aggregated append into the class lists
+        const unsigned want = __ballot_sync(0xffffffffu, cls >= 0);
+        if (want) {
+            const unsigned peers = __match_any_sync(0xffffffffu, cls);
+            if (cls >= 0) {
+                const int lane = threadIdx.x & 31;
+                const int leader = __ffs(peers) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(&a.list_count[cls], (unsigned long long)__popc(peers));
+                base = __shfl_sync(peers, base, leader);
+                const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
+                if (slot < a.list_cap) {
+                    a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | p;
+                    a.keys[cls][slot] = key;
+                }
+            }
+        }
+    }
+    if (stable) atomicAdd(&a.counters[CTR_STABLE], stable);
+    if (skipped) atomicAdd(&a.counters[CTR_BOUND], skipped);
+}
+
 template <int W, int R, int MODE>
 void launch_sim_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches, int* grid_out) {
     using TR = Traits<W, R, MODE>;
@@ -654,7 +724,7 @@ SimGeometry sim_geometry(int cls, int mode, int sm_count) {
     SimGeometry g{};
     int W = 32, R = 1;
     class_shape(cls, &W, &R);
-    if (mode != MODE_RANGE) W = 32;
+    if (mode == MODE_DEEP) W = 32;
     g.W = W;
     g.R = R;
     g.G = 32 / W;
@@ -701,23 +771,25 @@ void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t 
             case 5: launch_sim_t<32, 4, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
             case 6: launch_sim_t<32, 8, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
         }
-    } else if (mode == MODE_LIST) {
-        switch (cls) {
-            case 0: case 1: case 2: case 3: launch_sim_t<32, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
-            case 4: launch_sim_t<32, 2, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
-        }
     } else {
         switch (cls) {
-            case 0: launch_sim_t<4, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 1: launch_sim_t<8, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 2: launch_sim_t<16, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 3: launch_sim_t<32, 1, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 4: launch_sim_t<32, 2, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 5: launch_sim_t<32, 4, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
-            case 6: launch_sim_t<32, 8, MODE_RANGE>(a, sm_count, s, launches, grid_out); return;
+            case 0: launch_sim_t<4, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 1: launch_sim_t<8, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 2: launch_sim_t<16, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 3: launch_sim_t<32, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 4: launch_sim_t<32, 2, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 5: launch_sim_t<32, 4, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 6: launch_sim_t<32, 8, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
         }
     }
     throw EngineError(101, "unsupported JSQ kernel class");
+}
+
+void launch_plan_filter(const FilterArgs& a, cudaStream_t s, int* launches) {
+    if (a.nchunks == 0) return;
+    k_plan_filter<<<(unsigned)((a.nchunks + 127) / 128), 128, 0, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
 }
 
 void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches) {
