@@ -159,6 +159,43 @@ def run_reference(args):
     return 0
 
 
+def k1_at_scale(eng, torch, steps, warmup):
+    """The routing/aggregation pass (K1) on the C5 trace (10M requests, 4
+    stages, default decile grid) through cg_route_grid; K1's duration comes
+    from the engine's CUDA events around that kernel on its own stream."""
+    from paper_2506_04203_b200 import workloads as W
+    spec, seed = W.trace_specs("C5")[0]
+    t = eng.generate_trace(spec, seed)
+    n, C = int(t["arrival_s"].shape[0]), int(t["scores"].shape[0])
+    dev = {k: torch.from_numpy(np.ascontiguousarray(t[k])).cuda() for k in t}
+    tb = eng.TraceBuffers(dev["arrival_s"].data_ptr(), dev["input_tokens"].data_ptr(),
+                          dev["output_tokens"].data_ptr(), dev["scores"].data_ptr(), on_device=True,
+                          keep={"n": n, "stages": C, "t": dev})
+    E = eng.Engine(torch.cuda.current_device())
+    for _ in range(warmup):
+        E.route_grid(tb, {})
+    ms, launches = [], 0
+    for _ in range(steps):
+        E.route_grid(tb, {})
+        ms.append(E.last_stats["ms_k1"])
+        launches += E.last_stats["gpu_launches"]
+    bytes_per_launch = E.last_stats["k1_bytes"]
+    E.close()
+    del dev
+    torch.cuda.empty_cache()
+    return float(np.mean(ms)), bytes_per_launch, n, C, launches
+
+
+def committed_k1_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per K1 launch from the
+    committed ncu --set full capture summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 class _DevPtr:
     def __init__(self, ptr, nbytes):
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
@@ -249,10 +286,18 @@ def run_ours(args):
     value = plans * args.steps / (ms_dev / 1000.0)
     e2e = plans * args.steps / (ms_e2e / 1000.0)
 
+    k1 = None
+    if rank == 0 and not args.no_k1:
+        k1 = k1_at_scale(eng, torch, args.steps, args.warmup)
     if rank == 0:
         peak, peak_kind = load_peaks()
-        k1_ms = float(np.mean([s["ms_k1"] for s in st_dev]))
-        k1_bytes = st_dev[-1]["k1_bytes"]
+        if k1:
+            k1_ms, k1_bytes, k1_n, k1_C, k1_launches = k1
+            k1_work = f"C5 routing pass: {k1_n} requests x {k1_C} stages, default decile grid (cg_route_grid)"
+        else:
+            k1_ms = float(np.mean([s["ms_k1"] for s in st_dev]))
+            k1_bytes = st_dev[-1]["k1_bytes"]
+            k1_work = "C2 sweep routing pass"
         k1_gbs = k1_bytes / (k1_ms / 1000.0) / 1e9 if k1_ms > 0 else 0.0
         k4_ms = float(np.mean([s["ms_k4"] for s in st_dev]))
         steps_k4 = st_dev[-1]["request_steps"]
@@ -269,9 +314,10 @@ def run_ours(args):
                     "h2d_bytes_per_step": st_e2e[-1]["h2d_bytes"], "d2h_bytes_per_step": st_e2e[-1]["d2h_bytes"]},
             "gpu_launches": int(sum(s["gpu_launches"] for s in st_dev) + sum(s["gpu_launches"] for s in st_e2e)),
             "roofline": {"bound": "hbm", "kernel": "k_route_aggregate (K1 routing/aggregation pass)",
-                         "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": k1_gbs / peak if peak else None, "traffic": None,
-                         "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "ms_per_launch": k1_ms},
+                         "workload": k1_work, "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": k1_gbs / peak if peak else None, "traffic": committed_k1_traffic(),
+                         "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "ms_per_launch": k1_ms,
+                         "bytes_per_request": "16*C+8 (scores of C-1 threshold stages, input, C outputs, 8 B ranks)"},
             "roofline_k4": {"bound": "issue", "kernel": "k_sim (K4 JSQ simulation)", "ms_per_sweep": k4_ms,
                             "request_steps_per_s": steps_k4 / (k4_ms / 1000.0) if k4_ms > 0 else None,
                             "plans_simulated_full": st_dev[-1]["plans_simulated_full"],
@@ -305,6 +351,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOAD_DESC))
     ap.add_argument("--ref-grid", type=int, default=4, help="grid points per dim of the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-k1", action="store_true", help="skip the 10M-request K1 roofline pass")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -31,7 +31,9 @@ struct RouteArgs {
     unsigned long long* partials;  // [blocks][priv_words] block-private histograms (or null)
     long long max_partials;        // capacity of `partials` in blocks
     unsigned long long* acc;       // [priv_words] global accumulator (non-private path)
+    unsigned long long* tile_partials;  // [blocks][cells][2+C] for the tiled form (or null)
 };
+size_t tile_smem_bytes(long long cells, int D, int gtotal);
 
 struct WorkloadArgs {
     int C;
@@ -45,7 +47,9 @@ struct WorkloadArgs {
     unsigned long long* sum_out;
 };
 
-void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches);
+void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches,
+                            int* nblocks_out);
+void launch_hist_expand(const RouteArgs& a, int C, int nblocks, cudaStream_t s, int* launches);
 void launch_hist_scan(unsigned long long* hist, long long cells, int Q, const long long* stride,
                       const int* G, int D, cudaStream_t s, int* launches);
 void launch_workload_counts(const WorkloadArgs& a, cudaStream_t s, int* launches);

@@ -150,7 +150,7 @@ struct cg_engine {
     DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
     DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
-        d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
+        d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc;
 };
@@ -682,10 +682,15 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
                       ? E.d_partials.as<unsigned long long>((size_t)ra.max_partials * ra.priv_words)
                       : nullptr;
     ra.acc = E.d_acc.as<unsigned long long>((size_t)ra.priv_words);
+    ra.tile_partials = tile_smem_bytes(cells, D, ra.gtotal) <= 200 * 1024
+                           ? E.d_tpart.as<unsigned long long>((size_t)ra.max_partials * cells * Q)
+                           : nullptr;
     CG_CUDA(cudaMemsetAsync(ra.flags, 0, 4, x.s));
     CG_CUDA(cudaEventRecord(E.ev[0], x.s));
-    launch_route_aggregate(ra, D, E.sm_count, x.s, &x.launches);
+    int k1_blocks = 0;
+    launch_route_aggregate(ra, D, E.sm_count, x.s, &x.launches, &k1_blocks);
     CG_CUDA(cudaEventRecord(E.ev[1], x.s));
+    launch_hist_expand(ra, C, k1_blocks, x.s, &x.launches);
     launch_hist_scan(ra.hist, cells, Q, ra.stride, ra.G, D, x.s, &x.launches);
 
     // workloads per (stage, prefix)

@@ -228,6 +228,185 @@ __global__ void __launch_bounds__(256) k_route_aggregate(RouteArgs a) {
     }
 }
 
+// K1 (tiled form, used when the rank histogram fits in shared memory): per
+// tile of 2048 requests the block (512 threads, 4 requests each, 128-bit
+// loads) computes the rank cells, stores the packed ranks, stages the u32
+// tokens in shared memory and counting-sorts the tile by cell -- ONE 32-bit
+// shared atomic per request -- after which the owner thread of each cell adds
+// the cell's segment (count, sum_in, sum_out_0..C-1) into the block-private
+// u64 histogram without atomics.  The next tile's loads are issued before the
+// sort phases so HBM traffic overlaps them.
+constexpr int KT_THREADS = 512;
+constexpr int KT_TILE = 4 * KT_THREADS;
+
+template <int D>
+__global__ void __launch_bounds__(KT_THREADS, 1) k_route_tile(RouteArgs a) {
+    constexpr int C = D + 1;
+    constexpr int Q = 2 + C;
+    constexpr int NV = D + 1 + C;  // raw doubles per request
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const long long cells = a.cells;
+    unsigned long long* hist = reinterpret_cast<unsigned long long*>(smem_raw);             // [cells][Q]
+    unsigned* start = reinterpret_cast<unsigned*>(hist + cells * Q);                         // [cells+1]
+    unsigned* tcell = start + ((cells + 1 + 3) & ~3ll);                                      // [TILE]
+    unsigned* ttok = tcell + KT_TILE;                                                        // [C+1][TILE]
+    unsigned short* order = reinterpret_cast<unsigned short*>(ttok + (C + 1) * KT_TILE);    // [TILE]
+    double* s_grid = reinterpret_cast<double*>(order + KT_TILE + 8);
+    __shared__ unsigned wsum[KT_THREADS / 32];
+
+    for (int i = threadIdx.x; i < a.gtotal; i += KT_THREADS) s_grid[i] = a.gvals[i];
+    for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) hist[i] = 0ull;
+    const long long n = a.n;
+    const bool vec = (n & 1) == 0 && ((reinterpret_cast<unsigned long long>(a.scores) |
+                                        reinterpret_cast<unsigned long long>(a.in) |
+                                        reinterpret_cast<unsigned long long>(a.out) |
+                                        reinterpret_cast<unsigned long long>(a.ranks)) & 15ull) == 0;
+    const long long ntiles = (n + KT_TILE - 1) / KT_TILE;
+    bool bad = false;
+    // raw values of this thread's 4 requests: pairs at tile offsets 2*tid and 2*(tid+512)
+    double raw[4][NV];
+    auto load = [&](long long tile) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long r0 = tile * KT_TILE + 2 * (threadIdx.x + h * KT_THREADS);
+            if (vec && r0 + 1 < n) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const double* col = v < D ? a.scores + (long long)v * n
+                                              : (v == D ? a.in : a.out + (long long)(v - D - 1) * n);
+                    const double2 t = __ldcs(reinterpret_cast<const double2*>(col + r0));
+                    raw[2 * h][v] = t.x;
+                    raw[2 * h + 1][v] = t.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const long long r = r0 + e;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double* col = v < D ? a.scores + (long long)v * n
+                                                  : (v == D ? a.in : a.out + (long long)(v - D - 1) * n);
+                        raw[2 * h + e][v] = r < n ? col[r] : 0.0;
+                    }
+                }
+            }
+        }
+    };
+    long long tile = blockIdx.x;
+    if (tile < ntiles) load(tile);
+    __syncthreads();
+    for (; tile < ntiles; tile += gridDim.x) {
+        const long long tbase = tile * KT_TILE;
+        const int tlen = (int)((n - tbase) < KT_TILE ? (n - tbase) : KT_TILE);
+        // ---- ranks, cells, staged tokens
+        unsigned cell[4];
+        int li[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            li[q] = 2 * (threadIdx.x + (q >> 1) * KT_THREADS) + (q & 1);
+            unsigned long long pk = 0;
+            unsigned c = 0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int rk = rank_of(s_grid + a.goff[d], a.G[d], a.gtop[d], raw[q][d]);
+                pk |= (unsigned long long)rk << (16 * d);
+                c += (unsigned)rk * (unsigned)a.stride[d];
+            }
+            cell[q] = c;
+            const bool ve = li[q] < tlen;
+            if (ve) {
+                tcell[li[q]] = c;
+#pragma unroll
+                for (int v = 0; v <= C; ++v) ttok[v * KT_TILE + li[q]] = tok32(raw[q][D + v], bad);
+            }
+            raw[q][0] = __longlong_as_double((long long)pk);  // keep packed ranks for the store
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long r0 = tbase + 2 * (threadIdx.x + h * KT_THREADS);
+            const unsigned long long p0 = (unsigned long long)__double_as_longlong(raw[2 * h][0]);
+            const unsigned long long p1 = (unsigned long long)__double_as_longlong(raw[2 * h + 1][0]);
+            if (vec && r0 + 1 < n) {
+                *reinterpret_cast<ulonglong2*>(a.ranks + r0) = make_ulonglong2(p0, p1);
+            } else {
+                if (r0 < n) a.ranks[r0] = p0;
+                if (r0 + 1 < n) a.ranks[r0 + 1] = p1;
+            }
+        }
+        // ---- prefetch the next tile while this one is sorted and summed
+        if (tile + gridDim.x < ntiles) load(tile + gridDim.x);
+        for (long long i = threadIdx.x; i <= cells; i += KT_THREADS) start[i] = 0u;
+        __syncthreads();
+        unsigned rnk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            rnk[q] = li[q] < tlen ? atomicAdd(&start[cell[q]], 1u) : 0u;
+        __syncthreads();
+        // ---- exclusive scan of the per-cell counts (block-wide)
+        {
+            const long long per = (cells + KT_THREADS - 1) / KT_THREADS;
+            const long long lo = threadIdx.x * per;
+            const long long hi = lo + per < cells ? lo + per : cells;
+            unsigned tsum = 0;
+            for (long long i = lo; i < hi; ++i) tsum += start[i];
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            unsigned incl = tsum;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const unsigned v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            if (lane == 31) wsum[w] = incl;
+            __syncthreads();
+            unsigned wbase = 0;
+            for (int k = 0; k < w; ++k) wbase += wsum[k];
+            unsigned run = wbase + incl - tsum;
+            for (long long i = lo; i < hi; ++i) {
+                const unsigned v = start[i];
+                start[i] = run;
+                run += v;
+            }
+            if (threadIdx.x == KT_THREADS - 1) start[cells] = (unsigned)tlen;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (li[q] < tlen) order[start[cell[q]] + rnk[q]] = (unsigned short)li[q];
+        __syncthreads();
+        // ---- owner thread per cell: segmented sums, no atomics
+        for (long long c = threadIdx.x; c < cells; c += KT_THREADS) {
+            const unsigned b = start[c], e = start[c + 1];
+            if (b == e) continue;
+            unsigned long long acc[Q];
+            acc[0] = e - b;
+#pragma unroll
+            for (int v = 0; v <= C; ++v) acc[1 + v] = 0ull;
+            for (unsigned j = b; j < e; ++j) {
+                const int r = order[j];
+#pragma unroll
+                for (int v = 0; v <= C; ++v) acc[1 + v] += ttok[v * KT_TILE + r];
+            }
+            unsigned long long* hp = hist + c * Q;
+#pragma unroll
+            for (int v = 0; v < Q; ++v) hp[v] += acc[v];
+        }
+        __syncthreads();
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, 1u);
+    unsigned long long* part = a.tile_partials + (long long)blockIdx.x * cells * Q;
+    for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) part[i] = hist[i];
+}
+
+// Tiled form: partials are already [cells][Q]; sum over blocks.
+__global__ void k_hist_sum(const unsigned long long* __restrict__ part, long long len, int nblocks,
+                           unsigned long long* __restrict__ hist) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    unsigned long long s = 0;
+    for (int b = 0; b < nblocks; ++b) s += part[(long long)b * len + i];
+    hist[i] = s;
+}
+
 // Sum the block-private partials (or take the global accumulator) and expand
 // into the [cells][2+C] layout the dominance scan expects: the marginal sums
 // of stage i (i < C-1) sit at the cells whose dims >= i are at their maximum
@@ -465,8 +644,31 @@ __global__ void __launch_bounds__(QT_THREADS) k_quality(const double* __restrict
 
 }  // namespace
 
+size_t tile_smem_bytes(long long cells, int D, int gtotal) {
+    const int C = D + 1, Q = 2 + C;
+    return (size_t)cells * Q * 8 + (size_t)((cells + 1 + 3) & ~3ll) * 4 + (size_t)KT_TILE * 4 +
+           (size_t)(C + 1) * KT_TILE * 4 + (size_t)(KT_TILE + 8) * 2 + (size_t)gtotal * 8 + 64;
+}
+
 template <int D>
-void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches) {
+void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, int* nblocks_out) {
+    const size_t tsm = tile_smem_bytes(a.cells, D, a.gtotal);
+    if (a.tile_partials && tsm <= 200 * 1024) {
+        auto kern = k_route_tile<D>;
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        int per_sm = 0;
+        CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, KT_THREADS, tsm));
+        const long long ntiles = (a.n + KT_TILE - 1) / KT_TILE;
+        long long blocks = (long long)sm_count * (per_sm < 1 ? 1 : per_sm);
+        if (blocks > ntiles) blocks = ntiles;
+        if (blocks > a.max_partials) blocks = a.max_partials;
+        if (blocks < 1) blocks = 1;
+        kern<<<(unsigned)blocks, KT_THREADS, tsm, s>>>(a);
+        CG_LAUNCH_CHECK();
+        if (launches) *launches += 1;
+        if (nblocks_out) *nblocks_out = -(int)blocks;  // negative: tiled partial layout
+        return;
+    }
     const size_t grid_smem = a.grid_in_smem ? (size_t)a.gtotal * sizeof(double) : 0;
     const size_t hist_smem = (size_t)a.priv_words * 8;
     const bool priv = a.partials != nullptr && hist_smem + grid_smem <= 96 * 1024;
@@ -493,20 +695,33 @@ void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches) 
         k_route_aggregate<D, false><<<(unsigned)blocks, 256, grid_smem, s>>>(a);
     }
     CG_LAUNCH_CHECK();
-    k_hist_expand<<<(unsigned)((a.cells + 255) / 256), 256, 0, s>>>(a, D + 1, nb);
-    CG_LAUNCH_CHECK();
-    if (launches) *launches += 2;
+    if (launches) *launches += 1;
+    if (nblocks_out) *nblocks_out = nb;
 }
 
-void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches) {
+void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_t s, int* launches,
+                            int* nblocks_out) {
     switch (D) {
-        case 0: launch_k1<0>(a, sm_count, s, launches); break;
-        case 1: launch_k1<1>(a, sm_count, s, launches); break;
-        case 2: launch_k1<2>(a, sm_count, s, launches); break;
-        case 3: launch_k1<3>(a, sm_count, s, launches); break;
-        case 4: launch_k1<4>(a, sm_count, s, launches); break;
+        case 0: launch_k1<0>(a, sm_count, s, launches, nblocks_out); break;
+        case 1: launch_k1<1>(a, sm_count, s, launches, nblocks_out); break;
+        case 2: launch_k1<2>(a, sm_count, s, launches, nblocks_out); break;
+        case 3: launch_k1<3>(a, sm_count, s, launches, nblocks_out); break;
+        case 4: launch_k1<4>(a, sm_count, s, launches, nblocks_out); break;
         default: throw EngineError(101, "GPU engine supports up to 5 cascade stages");
     }
+}
+
+void launch_hist_expand(const RouteArgs& a, int C, int nblocks, cudaStream_t s, int* launches) {
+    if (nblocks < 0) {  // tiled form: [blocks][cells][2+C] partials -> hist
+        const long long len = a.cells * (2 + C);
+        k_hist_sum<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(a.tile_partials, len, -nblocks, a.hist);
+        CG_LAUNCH_CHECK();
+        if (launches) ++*launches;
+        return;
+    }
+    k_hist_expand<<<(unsigned)((a.cells + 255) / 256), 256, 0, s>>>(a, C, nblocks);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
 }
 
 void launch_hist_scan(unsigned long long* hist, long long cells, int Q, const long long* stride,
