@@ -239,15 +239,18 @@ __global__ void __launch_bounds__(256) k_route_aggregate(RouteArgs a) {
 constexpr int KT_THREADS = 512;
 constexpr int KT_TILE = 4 * KT_THREADS;
 
-template <int D>
+template <int D, bool GHIST>
 __global__ void __launch_bounds__(KT_THREADS, 1) k_route_tile(RouteArgs a) {
     constexpr int C = D + 1;
     constexpr int Q = 2 + C;
     constexpr int NV = D + 1 + C;  // raw doubles per request
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const long long cells = a.cells;
-    unsigned long long* hist = reinterpret_cast<unsigned long long*>(smem_raw);             // [cells][Q]
-    unsigned* start = reinterpret_cast<unsigned*>(hist + cells * Q);                         // [cells+1]
+    // block-private histogram: shared memory, or (GHIST, large grids) the
+    // block's own L2-resident slice of the partials -- owner-thread RMW, no atomics
+    unsigned long long* hist = GHIST ? a.tile_partials + (long long)blockIdx.x * cells * Q
+                                     : reinterpret_cast<unsigned long long*>(smem_raw);     // [cells][Q]
+    unsigned* start = reinterpret_cast<unsigned*>(smem_raw + (GHIST ? 0 : cells * Q * 8));   // [cells+1]
     unsigned* tcell = start + ((cells + 1 + 3) & ~3ll);                                      // [TILE]
     unsigned* ttok = tcell + KT_TILE;                                                        // [C+1][TILE]
     unsigned short* order = reinterpret_cast<unsigned short*>(ttok + (C + 1) * KT_TILE);    // [TILE]
@@ -255,7 +258,8 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_route_tile(RouteArgs a) {
     __shared__ unsigned wsum[KT_THREADS / 32];
 
     for (int i = threadIdx.x; i < a.gtotal; i += KT_THREADS) s_grid[i] = a.gvals[i];
-    for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) hist[i] = 0ull;
+    if (!GHIST)
+        for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) hist[i] = 0ull;
     const long long n = a.n;
     const bool vec = (n & 1) == 0 && ((reinterpret_cast<unsigned long long>(a.scores) |
                                         reinterpret_cast<unsigned long long>(a.in) |
@@ -393,8 +397,10 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_route_tile(RouteArgs a) {
         __syncthreads();
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, 1u);
-    unsigned long long* part = a.tile_partials + (long long)blockIdx.x * cells * Q;
-    for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) part[i] = hist[i];
+    if (!GHIST) {
+        unsigned long long* part = a.tile_partials + (long long)blockIdx.x * cells * Q;
+        for (long long i = threadIdx.x; i < cells * Q; i += KT_THREADS) part[i] = hist[i];
+    }
 }
 
 // Tiled form: partials are already [cells][Q]; sum over blocks.
@@ -644,17 +650,26 @@ __global__ void __launch_bounds__(QT_THREADS) k_quality(const double* __restrict
 
 }  // namespace
 
-size_t tile_smem_bytes(long long cells, int D, int gtotal) {
+size_t tile_smem_bytes(long long cells, int D, int gtotal, bool ghist) {
     const int C = D + 1, Q = 2 + C;
-    return (size_t)cells * Q * 8 + (size_t)((cells + 1 + 3) & ~3ll) * 4 + (size_t)KT_TILE * 4 +
+    return (ghist ? 0 : (size_t)cells * Q * 8) + (size_t)((cells + 1 + 3) & ~3ll) * 4 + (size_t)KT_TILE * 4 +
            (size_t)(C + 1) * KT_TILE * 4 + (size_t)(KT_TILE + 8) * 2 + (size_t)gtotal * 8 + 64;
+}
+
+// The histogram stays in shared memory while it is small; beyond that it moves
+// to the block's global (L2-resident) slice so more blocks fit per SM.
+bool tile_hist_global(long long cells, int D) { return (size_t)cells * (3 + D) * 8 > 120 * 1024; }
+
+size_t tile_smem_bytes(long long cells, int D, int gtotal) {
+    return tile_smem_bytes(cells, D, gtotal, tile_hist_global(cells, D));
 }
 
 template <int D>
 void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, int* nblocks_out) {
     const size_t tsm = tile_smem_bytes(a.cells, D, a.gtotal);
     if (a.tile_partials && tsm <= 200 * 1024) {
-        auto kern = k_route_tile<D>;
+        const bool ghist = tile_hist_global(a.cells, D);
+        auto kern = ghist ? k_route_tile<D, true> : k_route_tile<D, false>;
         CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         int per_sm = 0;
         CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, KT_THREADS, tsm));
@@ -663,6 +678,8 @@ void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, 
         if (blocks > ntiles) blocks = ntiles;
         if (blocks > a.max_partials) blocks = a.max_partials;
         if (blocks < 1) blocks = 1;
+        if (ghist)
+            CG_CUDA(cudaMemsetAsync(a.tile_partials, 0, (size_t)blocks * a.cells * (3 + D) * 8, s));
         kern<<<(unsigned)blocks, KT_THREADS, tsm, s>>>(a);
         CG_LAUNCH_CHECK();
         if (launches) *launches += 1;
