@@ -32,6 +32,13 @@ struct RouteArgs {
     long long max_partials;        // capacity of `partials` in blocks
     unsigned long long* acc;       // [priv_words] global accumulator (non-private path)
     unsigned long long* tile_partials;  // [blocks][cells][2+C] for the tiled form (or null)
+    // u32 form (k_route_hist): block-private u32 [cells][2+C] partials, the
+    // high 16 bits of tokens >= 2^16 accumulated in hi_acc (u64 [cells][2+C])
+    unsigned int* part32;
+    long long part32_words;        // capacity of part32
+    unsigned long long* hi_acc;
+    int bin_ok;                    // grid has no NaN: binned exact rank search allowed
+    int k1_form;                   // variant selector (engine option k1_form)
 };
 size_t tile_smem_bytes(long long cells, int D, int gtotal);
 

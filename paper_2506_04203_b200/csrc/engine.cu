@@ -140,6 +140,7 @@ struct cg_engine {
     cg_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
     int prune = 1;
+    int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
     long long tie_cap = 1 << 22;
@@ -152,7 +153,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc;
 };
 
 namespace {
@@ -685,6 +686,19 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
     ra.tile_partials = tile_smem_bytes(cells, D, ra.gtotal) <= 200 * 1024
                            ? E.d_tpart.as<unsigned long long>((size_t)ra.max_partials * cells * Q)
                            : nullptr;
+    {
+        // u32 form of K1: one u32 [cells][Q] slice per block (blocks handle <= 2^16 requests each)
+        bool nan = false;
+        for (double v : gv) nan |= (v != v);
+        ra.bin_ok = nan ? 0 : 1;
+        const long long blocks = std::max<long long>((long long)E.sm_count * 4, (n + 65535) / 65536 + E.sm_count);
+        ra.k1_form = E.k1_form;
+        if ((size_t)cells * Q * 4 <= 96 * 1024 && E.k1_form != 1) {
+            ra.part32_words = blocks * cells * Q;
+            ra.part32 = E.d_part32.as<unsigned int>((size_t)ra.part32_words);
+            ra.hi_acc = E.d_hiacc.as<unsigned long long>((size_t)cells * Q);
+        }
+    }
     CG_CUDA(cudaMemsetAsync(ra.flags, 0, 4, x.s));
     CG_CUDA(cudaEventRecord(E.ev[0], x.s));
     int k1_blocks = 0;
@@ -869,6 +883,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         if (!e || !key) fail(CG_ERR_INVALID_INPUT, "null engine/key");
         const std::string k(key);
         if (k == "prune") e->prune = value ? 1 : 0;
+        else if (k == "k1_form") e->k1_form = (int)value;
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);

@@ -29,6 +29,7 @@
 #include "cg_cuda.h"
 #include "cg_internal.h"
 #include "cg_kernels.h"
+#include "cg_ptx.cuh"
 
 namespace cg {
 
@@ -403,6 +404,359 @@ __global__ void __launch_bounds__(KT_THREADS, 1) k_route_tile(RouteArgs a) {
     }
 }
 
+// K1 (u32 form, used whenever the u32 cell histogram fits in shared memory).
+//
+// Rank search: per threshold dimension a 1024-bin table over the float image
+// of the distinct grid values.  bin(s) = clamp(floor((float(s) - lo) * sc))
+// is a composition of correctly rounded monotone operations, hence monotone
+// non-decreasing in s; so every grid value in a lower bin is <= s, every one
+// in a higher bin is > s, and only the values sharing s's bin need an exact
+// fp64 compare (normally at most one).  NaN scores land in bin 0 and compare
+// false: rank 0, as in the reference (`score >= h` is false).
+//
+// Aggregation: block-private u32 histogram [cells][2+C] (count, input sum,
+// output sums) in shared memory with native 32-bit shared atomics (64-bit
+// shared atomicAdd is a CAS loop on sm_100).  A block handles at most 2^16
+// requests, so counts and sums of the low 16 bits of every token are exact in
+// u32; the (rare) high parts of tokens >= 2^16 go to a global u64 accumulator.
+constexpr int KH_THREADS = 512;
+constexpr int KH_NB = 1024;                         // bins per dimension
+constexpr int KH_MAX_REQ = 65536;                   // requests per block
+constexpr int KH_MAX_ITERS = KH_MAX_REQ / (2 * KH_THREADS);
+
+__device__ __forceinline__ int bin_of(double s, float lo, float sc) {
+    const float f = __double2float_rn(s);
+    const int b = __float2int_rd(__fmul_rn(__fsub_rn(f, lo), sc));  // NaN -> 0
+    return min(max(b, 0), KH_NB - 1);
+}
+
+__device__ __forceinline__ void bin_params(const double* v, int g, float& lo, float& sc) {
+    if (g <= 0) {
+        lo = 0.f;
+        sc = 0.f;
+        return;
+    }
+    lo = __double2float_rn(v[0]);
+    const float hi = __double2float_rn(v[g - 1]);
+    const float span = __fsub_rn(hi, lo);
+    sc = span > 0.f ? __fdiv_rn((float)(KH_NB - 1), span) : 0.f;
+    if (!(sc == sc) || sc < 0.f) sc = 0.f;  // inf span etc.: one bin (still exact)
+}
+
+__device__ __forceinline__ int rank_binned(const double* __restrict__ v, const unsigned* __restrict__ tab,
+                                           int g, float lo, float sc, double s) {
+    const unsigned e = tab[bin_of(s, lo, sc)];
+    const int j0 = (int)(e & 0xffffu);
+    const int c = (int)(e >> 16);
+    int r = j0;
+    if (c > 0) r += (v[j0] <= s) ? 1 : 0;
+    if (c > 1) {
+        for (int k = 1; k < c; ++k) r += (v[j0 + k] <= s) ? 1 : 0;
+    }
+    return r;
+}
+
+// Per-dimension bin tables (all threads of the block call this; s_grid must
+// be filled and visible): tab[d][b] = j0(b) | (j0(b+1) - j0(b)) << 16 with
+// j0(b) = #{j : bin(v_j) < b}.
+template <int D>
+__device__ __forceinline__ void build_bin_tables(const RouteArgs& a, const double* s_grid, unsigned* tab,
+                                                 int* s_bin /*[32]*/, float* lo, float* sc, int nthreads) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) bin_params(a.gvals + a.goff[d], a.G[d], lo[d], sc[d]);
+    __syncthreads();
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+        const double* v = s_grid + a.goff[d];
+        const int g = a.G[d];
+        unsigned* t = tab + d * (KH_NB + 1);
+        if (g <= 32) {
+            for (int j = threadIdx.x; j < g; j += nthreads) s_bin[j] = bin_of(v[j], lo[d], sc[d]);
+            __syncthreads();
+            for (int b = threadIdx.x; b < KH_NB; b += nthreads) {
+                int j0 = 0, j1 = 0;
+                for (int j = 0; j < g; ++j) {
+                    j0 += s_bin[j] < b ? 1 : 0;
+                    j1 += s_bin[j] <= b ? 1 : 0;
+                }
+                t[b] = (unsigned)j0 | ((unsigned)(j1 - j0) << 16);
+            }
+            __syncthreads();
+        } else {
+            for (int b = threadIdx.x; b < KH_NB; b += nthreads) {
+                // binary searches over the monotone bins of the sorted values
+                int l0 = 0, h0 = g;
+                while (l0 < h0) {
+                    const int m = (l0 + h0) >> 1;
+                    if (bin_of(v[m], lo[d], sc[d]) < b) l0 = m + 1; else h0 = m;
+                }
+                int l1 = l0, h1 = g;
+                while (l1 < h1) {
+                    const int m = (l1 + h1) >> 1;
+                    if (bin_of(v[m], lo[d], sc[d]) <= b) l1 = m + 1; else h1 = m;
+                }
+                t[b] = (unsigned)l0 | ((unsigned)(l1 - l0) << 16);
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// One request into the block-private u32 histogram (see k_route_hist).
+template <int C>
+__device__ __forceinline__ void hist32_add(unsigned* __restrict__ hist, unsigned long long* __restrict__ hi_acc,
+                                           unsigned cell, const double* tokd /*[C+1]: in, out_0..*/, bool& bad) {
+    constexpr int Q = 2 + C;
+    unsigned* hp = hist + (unsigned long long)cell * Q;
+    unsigned tk[C + 1];
+#pragma unroll
+    for (int v = 0; v <= C; ++v) tk[v] = tok32(tokd[v], bad);
+    atomicAdd(&hp[0], 1u);
+#pragma unroll
+    for (int v = 0; v <= C; ++v) {
+        atomicAdd(&hp[1 + v], tk[v] & 0xffffu);
+        if (tk[v] >> 16)
+            atomicAdd(&hi_acc[(unsigned long long)cell * Q + 1 + v], (unsigned long long)(tk[v] & 0xffff0000u));
+    }
+}
+
+template <int D, int MINB>
+__global__ void __launch_bounds__(KH_THREADS, MINB) k_route_hist(RouteArgs a) {
+    constexpr int C = D + 1;
+    constexpr int Q = 2 + C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const long long cells = a.cells;
+    unsigned* hist = reinterpret_cast<unsigned*>(smem_raw);                       // [cells][Q]
+    const long long hw = (cells * Q + 3) & ~3ll;
+    unsigned* tab = hist + hw;                                                    // [D][NB+1]
+    double* s_grid = reinterpret_cast<double*>(tab + ((D * (KH_NB + 1) + 3) & ~3));  // [gtotal]
+    __shared__ int s_bin[32];  // scratch: bins of grid values while building a table
+
+    for (int i = threadIdx.x; i < a.gtotal; i += KH_THREADS) s_grid[i] = a.gvals[i];
+    for (long long i = threadIdx.x; i < hw; i += KH_THREADS) hist[i] = 0u;
+    float lo[D > 0 ? D : 1], sc[D > 0 ? D : 1];
+    build_bin_tables<D>(a, s_grid, tab, s_bin, lo, sc, KH_THREADS);
+
+    bool bad = false;
+    const long long n = a.n;
+    const long long npairs = (n + 1) >> 1;
+    const bool vec = (n & 1) == 0 && ((reinterpret_cast<unsigned long long>(a.scores) |
+                                        reinterpret_cast<unsigned long long>(a.in) |
+                                        reinterpret_cast<unsigned long long>(a.out) |
+                                        reinterpret_cast<unsigned long long>(a.ranks)) & 15ull) == 0;
+    const long long stride = (long long)gridDim.x * KH_THREADS;
+    const long long first = blockIdx.x * (long long)KH_THREADS + threadIdx.x;
+    const long long iters = (npairs - first + stride - 1) / stride;  // this thread's pairs (may be <= 0)
+    double nsc[D > 0 ? D : 1][2], nxin[2], nxo[C][2];
+    auto load_pair = [&](long long r0) {
+        if (vec && r0 + 1 < n) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const double2 t = __ldcs(reinterpret_cast<const double2*>(a.scores + (long long)d * n + r0));
+                nsc[d][0] = t.x;
+                nsc[d][1] = t.y;
+            }
+            const double2 ti = __ldcs(reinterpret_cast<const double2*>(a.in + r0));
+            nxin[0] = ti.x;
+            nxin[1] = ti.y;
+#pragma unroll
+            for (int i = 0; i < C; ++i) {
+                const double2 t = __ldcs(reinterpret_cast<const double2*>(a.out + (long long)i * n + r0));
+                nxo[i][0] = t.x;
+                nxo[i][1] = t.y;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long r = r0 + e;
+                const bool ve = r < n;
+#pragma unroll
+                for (int d = 0; d < D; ++d) nsc[d][e] = ve ? a.scores[(long long)d * n + r] : 0.0;
+                nxin[e] = ve ? a.in[r] : 0.0;
+#pragma unroll
+                for (int i = 0; i < C; ++i) nxo[i][e] = ve ? a.out[(long long)i * n + r] : 0.0;
+            }
+        }
+    };
+    if (iters > 0) load_pair(2 * first);
+    for (long long it = 0; it < iters; ++it) {
+        const long long r0 = 2 * (first + it * stride);
+        double sc_[D > 0 ? D : 1][2], xin[2], xo[C][2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) sc_[d][e] = nsc[d][e];
+            xin[e] = nxin[e];
+#pragma unroll
+            for (int i = 0; i < C; ++i) xo[i][e] = nxo[i][e];
+        }
+        if (it + 1 < iters) load_pair(r0 + 2 * stride);
+        unsigned long long pk[2] = {0ull, 0ull};
+        unsigned cell[2] = {0u, 0u};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int rk = a.bin_ok ? rank_binned(s_grid + a.goff[d], tab + d * (KH_NB + 1), a.G[d], lo[d],
+                                                      sc[d], sc_[d][e])
+                                        : rank_of(s_grid + a.goff[d], a.G[d], a.gtop[d], sc_[d][e]);
+                pk[e] |= (unsigned long long)rk << (16 * d);
+                cell[e] += (unsigned)rk * (unsigned)a.stride[d];
+            }
+        }
+        const bool v1 = r0 + 1 < n;
+        if (v1 && vec) {
+            __stcs(reinterpret_cast<ulonglong2*>(a.ranks + r0), make_ulonglong2(pk[0], pk[1]));
+        } else {
+            a.ranks[r0] = pk[0];
+            if (v1) a.ranks[r0 + 1] = pk[1];
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            if (e == 1 && !v1) break;
+            unsigned* hp = hist + (unsigned long long)cell[e] * Q;
+            unsigned tk[C + 1];
+            tk[0] = tok32(xin[e], bad);
+#pragma unroll
+            for (int i = 0; i < C; ++i) tk[1 + i] = tok32(xo[i][e], bad);
+            atomicAdd(&hp[0], 1u);
+#pragma unroll
+            for (int v = 0; v <= C; ++v) {
+                atomicAdd(&hp[1 + v], tk[v] & 0xffffu);
+                if (tk[v] >> 16)
+                    atomicAdd(&a.hi_acc[(unsigned long long)cell[e] * Q + 1 + v],
+                              (unsigned long long)(tk[v] & 0xffff0000u));
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, 1u);
+    __syncthreads();
+    unsigned* part = a.part32 + (long long)blockIdx.x * cells * Q;
+    for (long long i = threadIdx.x; i < cells * Q; i += KH_THREADS) __stcg(part + i, hist[i]);
+}
+
+
+// K1, TMA-ring form (the default when the trace columns are 16-byte aligned
+// and n is even).  One producer warp streams tiles of KR_T requests of every
+// SoA column (C-1 score columns, input, C output columns) into a KR_STAGES
+// shared-memory ring with cp.async.bulk (UBLKCP) and mbarrier transaction
+// counts; KR_NWC consumer warps route one request per thread per tile from
+// shared memory, release the slot as soon as the values are in registers, and
+// aggregate into the block-private u32 histogram exactly as k_route_hist.  No
+// register double-buffering: the bytes in flight live in the ring.
+constexpr int KR_NWC = 8;
+constexpr int KR_T = 32 * KR_NWC;
+constexpr int KR_STAGES = 3;
+constexpr int KR_THREADS = 32 * (KR_NWC + 1);
+constexpr int KR_MAX_TILES = KH_MAX_REQ / KR_T;     // per block: u32 sums stay exact
+
+template <int D>
+struct KRLayout {
+    static constexpr int C = D + 1;
+    static constexpr int NV = D + 1 + C;            // columns per request
+    static constexpr size_t ring_bytes = (size_t)KR_STAGES * NV * KR_T * 8;
+};
+
+template <int D>
+__global__ void __launch_bounds__(KR_THREADS, 1) k_route_tma(RouteArgs a, long long tiles_per_block) {
+    constexpr int C = D + 1;
+    constexpr int Q = 2 + C;
+    constexpr int NV = KRLayout<D>::NV;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* ring = reinterpret_cast<double*>(smem_raw);                            // [S][NV][T]
+    const long long cells = a.cells;
+    unsigned* hist = reinterpret_cast<unsigned*>(smem_raw + KRLayout<D>::ring_bytes);  // [cells][Q]
+    const long long hw = (cells * Q + 3) & ~3ll;
+    unsigned* tab = hist + hw;                                                     // [D][NB+1]
+    double* s_grid = reinterpret_cast<double*>(tab + ((D * (KH_NB + 1) + 3) & ~3));   // [gtotal]
+    __shared__ __align__(8) unsigned long long full_bar[KR_STAGES], empty_bar[KR_STAGES];
+    __shared__ int s_bin[32];
+
+    const long long n = a.n;
+    const long long ntiles = (n + KR_T - 1) / KR_T;
+    const long long t0 = blockIdx.x * tiles_per_block;
+    const long long t1 = min(ntiles, t0 + tiles_per_block);
+    const long long my_tiles = t1 > t0 ? t1 - t0 : 0;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < KR_STAGES; ++st) {
+            mbar_init(&full_bar[st], 1);
+            mbar_init(&empty_bar[st], KR_NWC);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < a.gtotal; i += KR_THREADS) s_grid[i] = a.gvals[i];
+    for (long long i = threadIdx.x; i < hw; i += KR_THREADS) hist[i] = 0u;
+    float lo[D > 0 ? D : 1], sc[D > 0 ? D : 1];
+    build_bin_tables<D>(a, s_grid, tab, s_bin, lo, sc, KR_THREADS);  // ends with __syncthreads
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == KR_NWC) {
+        // ---------------- producer
+        if (lane == 0) {
+            const unsigned long long pol = l2_evict_first_policy();
+            for (long long i = 0; i < my_tiles; ++i) {
+                const int st = (int)(i % KR_STAGES);
+                if (i >= KR_STAGES) mbar_wait(&empty_bar[st], (unsigned)(((i / KR_STAGES) - 1) & 1));
+                const long long base = (t0 + i) * KR_T;
+                const long long len = min((long long)KR_T, n - base);
+                const unsigned bytes = (unsigned)(len * 8);
+                mbar_arrive_expect_tx(&full_bar[st], bytes * NV);
+                double* dst = ring + (size_t)st * NV * KR_T;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const double* col = v < D ? a.scores + (long long)v * n
+                                              : (v == D ? a.in : a.out + (long long)(v - D - 1) * n);
+                    bulk_g2s(dst + v * KR_T, col + base, bytes, &full_bar[st], pol);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers
+    bool bad = false;
+    for (long long i = 0; i < my_tiles; ++i) {
+        const int st = (int)(i % KR_STAGES);
+        const long long base = (t0 + i) * KR_T;
+        const int len = (int)min((long long)KR_T, n - base);
+        mbar_wait(&full_bar[st], (unsigned)((i / KR_STAGES) & 1));
+        const double* src = ring + (size_t)st * NV * KR_T + threadIdx.x;
+        double x[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) x[v] = src[v * KR_T];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+        if ((int)threadIdx.x < len) {
+            unsigned long long pk = 0;
+            unsigned cell = 0;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const int rk = a.bin_ok ? rank_binned(s_grid + a.goff[d], tab + d * (KH_NB + 1), a.G[d], lo[d],
+                                                      sc[d], x[d])
+                                        : rank_of(s_grid + a.goff[d], a.G[d], a.gtop[d], x[d]);
+                pk |= (unsigned long long)rk << (16 * d);
+                cell += (unsigned)rk * (unsigned)a.stride[d];
+            }
+            a.ranks[base + threadIdx.x] = pk;
+            hist32_add<C>(hist, a.hi_acc, cell, x + D, bad);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flags, 1u);
+    named_bar_sync(1, KR_NWC * 32);
+    unsigned* part = a.part32 + (long long)blockIdx.x * cells * Q;
+    for (long long i = threadIdx.x; i < cells * Q; i += KR_NWC * 32) __stcg(part + i, hist[i]);
+}
+
+// u32 form: hist = sum over blocks of the u32 partials + the high-part accumulator.
+__global__ void k_hist_sum32(const unsigned* __restrict__ part, long long len, int nblocks,
+                             const unsigned long long* __restrict__ hi, unsigned long long* __restrict__ hist) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    unsigned long long s = hi[i];
+    for (int b = 0; b < nblocks; ++b) s += __ldcs(part + (long long)b * len + i);
+    hist[i] = s;
+}
+
 // Tiled form: partials are already [cells][Q]; sum over blocks.
 __global__ void k_hist_sum(const unsigned long long* __restrict__ part, long long len, int nblocks,
                            unsigned long long* __restrict__ hist) {
@@ -664,8 +1018,64 @@ size_t tile_smem_bytes(long long cells, int D, int gtotal) {
     return tile_smem_bytes(cells, D, gtotal, tile_hist_global(cells, D));
 }
 
+size_t hist32_smem_bytes(long long cells, int D, int gtotal) {
+    const int Q = 3 + D;
+    return (size_t)((cells * Q + 3) & ~3ll) * 4 + (size_t)((D * (KH_NB + 1) + 3) & ~3) * 4 + (size_t)gtotal * 8;
+}
+
 template <int D>
 void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, int* nblocks_out) {
+    const size_t hsm = hist32_smem_bytes(a.cells, D, a.gtotal);
+    const size_t tsm_r = KRLayout<D>::ring_bytes + hsm;
+    const bool aligned = (a.n & 1) == 0 && ((reinterpret_cast<unsigned long long>(a.scores) |
+                                             reinterpret_cast<unsigned long long>(a.in) |
+                                             reinterpret_cast<unsigned long long>(a.out)) & 15ull) == 0;
+    if (a.part32 && a.hi_acc && aligned && a.k1_form == 0 && tsm_r <= 200 * 1024 && a.n > 0) {
+        auto kern = k_route_tma<D>;
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm_r));
+        int per_sm = 0;
+        CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, KR_THREADS, tsm_r));
+        const long long cap = (long long)sm_count * (per_sm < 1 ? 1 : per_sm);
+        const long long ntiles = (a.n + KR_T - 1) / KR_T;
+        long long tpb = (ntiles + cap - 1) / cap;
+        if (tpb > KR_MAX_TILES) {  // more than one wave: equal waves of full-size blocks
+            const long long waves = (ntiles + cap * KR_MAX_TILES - 1) / (cap * KR_MAX_TILES);
+            tpb = (ntiles + cap * waves - 1) / (cap * waves);
+        }
+        if (tpb < 1) tpb = 1;
+        const long long blocks = (ntiles + tpb - 1) / tpb;
+        const long long Q = 3 + D;
+        if (blocks * a.cells * Q <= a.part32_words) {
+            CG_CUDA(cudaMemsetAsync(a.hi_acc, 0, (size_t)a.cells * Q * 8, s));
+            kern<<<(unsigned)blocks, KR_THREADS, tsm_r, s>>>(a, tpb);
+            CG_LAUNCH_CHECK();
+            if (launches) *launches += 1;
+            if (nblocks_out) *nblocks_out = -(int)blocks - (1 << 24);  // u32 partial layout
+            return;
+        }
+    }
+    if (a.part32 && a.hi_acc && hsm <= 110 * 1024) {
+        auto kern = a.k1_form == 3 ? k_route_hist<D, 1> : k_route_hist<D, 2>;
+        CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+        int per_sm = 0;
+        CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, KH_THREADS, hsm));
+        const long long npairs = (a.n + 1) / 2;
+        long long blocks = (long long)sm_count * (per_sm < 1 ? 1 : per_sm);
+        const long long need = (npairs + (long long)KH_MAX_ITERS * KH_THREADS - 1) / ((long long)KH_MAX_ITERS * KH_THREADS);
+        const long long useful = (npairs + KH_THREADS - 1) / KH_THREADS;
+        if (blocks > useful) blocks = useful;
+        if (blocks < need) blocks = need;
+        if (blocks < 1) blocks = 1;
+        const long long Q = 3 + D;
+        if (blocks * a.cells * Q <= a.part32_words) {
+            CG_CUDA(cudaMemsetAsync(a.hi_acc, 0, (size_t)a.cells * Q * 8, s));
+            kern<<<(unsigned)blocks, KH_THREADS, hsm, s>>>(a);
+            CG_LAUNCH_CHECK();
+            if (launches) *launches += 1;
+            if (nblocks_out) *nblocks_out = -(int)blocks - (1 << 24);  // u32 partial layout
+            return;
+        }
+    }
     const size_t tsm = tile_smem_bytes(a.cells, D, a.gtotal);
     if (a.tile_partials && tsm <= 200 * 1024) {
         const bool ghist = tile_hist_global(a.cells, D);
@@ -729,6 +1139,14 @@ void launch_route_aggregate(const RouteArgs& a, int D, int sm_count, cudaStream_
 }
 
 void launch_hist_expand(const RouteArgs& a, int C, int nblocks, cudaStream_t s, int* launches) {
+    if (nblocks <= -(1 << 24)) {  // u32 form: [blocks][cells][2+C] u32 partials + high parts -> hist
+        const long long len = a.cells * (2 + C);
+        const int nb = -(nblocks + (1 << 24));
+        k_hist_sum32<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(a.part32, len, nb, a.hi_acc, a.hist);
+        CG_LAUNCH_CHECK();
+        if (launches) ++*launches;
+        return;
+    }
     if (nblocks < 0) {  // tiled form: [blocks][cells][2+C] partials -> hist
         const long long len = a.cells * (2 + C);
         k_hist_sum<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(a.tile_partials, len, -nblocks, a.hist);
