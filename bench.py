@@ -313,7 +313,7 @@ def run_ours(args):
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
                     "h2d_bytes_per_step": st_e2e[-1]["h2d_bytes"], "d2h_bytes_per_step": st_e2e[-1]["d2h_bytes"]},
             "gpu_launches": int(sum(s["gpu_launches"] for s in st_dev) + sum(s["gpu_launches"] for s in st_e2e)),
-            "roofline": {"bound": "hbm", "kernel": "k_route_aggregate (K1 routing/aggregation pass)",
+            "roofline": {"bound": "hbm", "kernel": "k_route_tma (K1 routing/aggregation pass: cp.async.bulk ring + u32 smem histogram)",
                          "workload": k1_work, "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
                          "frac": k1_gbs / peak if peak else None, "traffic": committed_k1_traffic(),
                          "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "ms_per_launch": k1_ms,

@@ -700,6 +700,7 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
         }
     }
     CG_CUDA(cudaMemsetAsync(ra.flags, 0, 4, x.s));
+    if (ra.hi_acc) CG_CUDA(cudaMemsetAsync(ra.hi_acc, 0, (size_t)cells * Q * 8, x.s));
     CG_CUDA(cudaEventRecord(E.ev[0], x.s));
     int k1_blocks = 0;
     launch_route_aggregate(ra, D, E.sm_count, x.s, &x.launches, &k1_blocks);

@@ -1045,8 +1045,7 @@ void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, 
         if (tpb < 1) tpb = 1;
         const long long blocks = (ntiles + tpb - 1) / tpb;
         const long long Q = 3 + D;
-        if (blocks * a.cells * Q <= a.part32_words) {
-            CG_CUDA(cudaMemsetAsync(a.hi_acc, 0, (size_t)a.cells * Q * 8, s));
+        if (blocks * a.cells * Q <= a.part32_words) {  // hi_acc is zeroed by the caller
             kern<<<(unsigned)blocks, KR_THREADS, tsm_r, s>>>(a, tpb);
             CG_LAUNCH_CHECK();
             if (launches) *launches += 1;
@@ -1067,8 +1066,7 @@ void launch_k1(const RouteArgs& a, int sm_count, cudaStream_t s, int* launches, 
         if (blocks < need) blocks = need;
         if (blocks < 1) blocks = 1;
         const long long Q = 3 + D;
-        if (blocks * a.cells * Q <= a.part32_words) {
-            CG_CUDA(cudaMemsetAsync(a.hi_acc, 0, (size_t)a.cells * Q * 8, s));
+        if (blocks * a.cells * Q <= a.part32_words) {  // hi_acc is zeroed by the caller
             kern<<<(unsigned)blocks, KH_THREADS, hsm, s>>>(a);
             CG_LAUNCH_CHECK();
             if (launches) *launches += 1;

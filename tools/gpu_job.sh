@@ -18,6 +18,6 @@ if [[ $what == *ncu* ]]; then
       python tools/perf_probe.py C2 - 1 > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 8 \
       -o gpurun_out/prof_k4_c2 -f python tools/perf_probe.py C2 - 1 1 > gpurun_out/ncu_k4.log 2>&1; echo "ncu k4 rc=$?"
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_route_(tile|aggregate)" -s 1 -c 1 \
-      -o gpurun_out/prof_k1_c5 -f python tools/k1_probe.py C5 2 > gpurun_out/ncu_k1.log 2>&1; echo "ncu k1 rc=$?"
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_route_(tma|hist|tile|aggregate)" -s 1 -c 1 \
+      -o gpurun_out/prof_k1_c5 -f python tools/k1_probe.py C5 3 > gpurun_out/ncu_k1.log 2>&1; echo "ncu k1 rc=$?"
 fi
