@@ -17,6 +17,8 @@
  *                            include/cascade/innerplan.hpp:63, src/innerplan.cpp:131-194
  *   cg_generate_trace     <- cascade::cli::generate_trace (synthetic input only)
  *                            include/cascade/cli.hpp:171-172, src/cli.cpp:428-460
+ *   cg_read_trace_jsonl   <- cascade::read_trace_jsonl (trace ingest)
+ *                            include/cascade/domain.hpp:162, src/domain.cpp:361-387
  *
  * Conventions
  *   - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
@@ -290,6 +292,36 @@ cg_status cg_solve_min_max(cg_engine* engine, const double* entries, int32_t sta
 cg_status cg_generate_trace(const char* spec_json, uint64_t seed, double* arrival_s,
                             double* input_tokens, double* output_tokens, double* scores,
                             int64_t capacity, int64_t* n_out, int32_t* stages_out);
+
+/* Trace ingest: cascade::read_trace_jsonl (domain.cpp:361-387) on the GPU.
+ * The JSONL bytes are split, parsed, validated (require_valid per record,
+ * non-decreasing arrivals) and decoded into SoA columns in HBM.  Errors carry
+ * the reference's Errc and exact message (io_error "cannot open trace file:
+ * <path>", invalid_input "<path>:<line>: bad trace record: <json what()>",
+ * "invalid TraceRecord: ...;", "<path>:<line>: arrival times must be
+ * non-decreasing").  An empty file (or only empty lines) yields n = 0. */
+typedef struct cg_ingest_stats {
+    int64_t bytes;
+    int64_t lines;
+    int64_t records;
+    int64_t host_lines;      /* lines the device parser left to the host JSON decoder */
+    int32_t gpu_launches;
+    double ms_total;         /* host wall time of the call (file read excluded) */
+    double ms_read;          /* file read into pinned memory (cg_read_trace_jsonl) */
+} cg_ingest_stats;
+
+typedef struct cg_trace_buffer {
+    cg_trace host;           /* host SoA columns, owned by this buffer */
+    cg_trace device;         /* the same columns in HBM (on_device = 1), owned by the
+                                engine: valid until its next ingest call or destroy */
+    cg_ingest_stats stats;
+} cg_trace_buffer;
+
+cg_status cg_read_trace_jsonl(cg_engine* engine, const char* path, cg_trace_buffer** out);
+/* Same on an in-memory file image; `path` is used in error messages only. */
+cg_status cg_parse_trace_jsonl(cg_engine* engine, const char* bytes, int64_t len, const char* path,
+                               cg_trace_buffer** out);
+void cg_trace_buffer_free(cg_trace_buffer* buffer);
 
 const char* cg_version(void);
 

@@ -1,6 +1,7 @@
-// Drop-in check: the reference planner with cascade::outerplan::sweep served
-// by the GPU engine (integration/outerplan_gpu.cpp) vs. the reference's own
-// CPU body (outerplan.cpp compiled with -Dsweep=cpu_sweep, see
+// Drop-in check: the reference planner with cascade::outerplan::sweep and
+// cascade::read_trace_jsonl served by the GPU engine (integration/*_gpu.cpp)
+// vs. the reference's own CPU bodies (outerplan.cpp / domain.cpp compiled
+// with -Dsweep=cpu_sweep / -Dread_trace_jsonl=cpu_read_trace_jsonl, see
 // oracle/Makefile target `dropin`).  Runs the CLI's plan pipeline and
 // compares the output files byte for byte.
 //
@@ -18,6 +19,9 @@
 #include "cascade/cli.hpp"
 #include "cascade/outerplan.hpp"
 
+namespace cascade {
+std::vector<TraceRecord> cpu_read_trace_jsonl(const std::string& path);
+}
 namespace cascade::outerplan {
 SweepResult cpu_sweep(const std::vector<TraceRecord>& trace, const std::vector<ModelSpec>& models,
                       const HardwareSpec& hw, const costmodel::CostModelParams& params, int total_gpus,
@@ -62,7 +66,13 @@ int main(int argc, char** argv) {
 
     // CPU: the reference's own sweep body, same writers as cmd_plan.
     auto cfg = cli::load_planner_config(cfg_path);
-    auto tr = read_trace_jsonl(trace_path);
+    t0 = std::chrono::steady_clock::now();
+    auto tr = cpu_read_trace_jsonl(trace_path);
+    const double cpu_read_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    t0 = std::chrono::steady_clock::now();
+    auto tr_gpu = read_trace_jsonl(trace_path);
+    const double gpu_read_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const bool trace_identical = tr_gpu == tr;
     t0 = std::chrono::steady_clock::now();
     auto res = outerplan::cpu_sweep(tr, cfg.models, cfg.hardware, cfg.cost_model, cfg.hardware.gpu_count, cfg.sweep);
     const double cpu_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -81,6 +91,10 @@ int main(int argc, char** argv) {
         report["files"][f] = {{"identical", a == b}, {"bytes", a.size()}};
         all = all && a == b;
     }
+    all = all && trace_identical;
+    report["trace_identical"] = trace_identical;
+    report["gpu_read_s"] = gpu_read_s;
+    report["cpu_read_s"] = cpu_read_s;
     report["identical"] = all;
     report["gpu_s"] = gpu_s;
     report["cpu_s"] = cpu_s;

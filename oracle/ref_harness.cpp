@@ -12,6 +12,7 @@
 //   cascade::costmodel::StageEvaluator::row  proj/include/cascade/costmodel.hpp:110-111
 //   cascade::innerplan::solve_min_max    proj/include/cascade/innerplan.hpp:63
 //   cascade::cli::generate_trace         proj/include/cascade/cli.hpp:171-172
+//   cascade::read_trace_jsonl / write_trace_jsonl  proj/include/cascade/domain.hpp:162-164
 //
 // Every function returns a malloc'd JSON string (free with ref_free):
 //   {"ok":true,"result":<reference to_json of the result>,"elapsed_s":t}
@@ -47,7 +48,7 @@ char* ok(json result, double elapsed) {
     j["ok"] = true;
     j["result"] = std::move(result);
     j["elapsed_s"] = elapsed;
-    return dup(j.dump());
+    return dup(j.dump(-1, ' ', false, json::error_handler_t::replace));
 }
 
 char* fail(const CascadeError& e) {
@@ -56,7 +57,7 @@ char* fail(const CascadeError& e) {
     j["code"] = static_cast<int>(e.code());
     j["code_name"] = e.code_name();
     j["message"] = e.what();
-    return dup(j.dump());
+    return dup(j.dump(-1, ' ', false, json::error_handler_t::replace));
 }
 
 char* fail_std(const std::exception& e) {
@@ -65,7 +66,7 @@ char* fail_std(const std::exception& e) {
     j["code"] = 100;
     j["code_name"] = "STD_EXCEPTION";
     j["message"] = e.what();
-    return dup(j.dump());
+    return dup(j.dump(-1, ' ', false, json::error_handler_t::replace));
 }
 
 std::vector<TraceRecord> make_trace(const double* arrival, const double* in_tok,
@@ -253,6 +254,46 @@ char* ref_generate_trace(const char* spec_json, std::uint64_t seed, double* arri
             }
         }
         return ok(json(n), 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// write_trace_jsonl (domain.cpp:389-394) of SoA columns.
+char* ref_write_trace_jsonl(const double* arrival, const double* in_tok, const double* out_tok,
+                            const double* scores, std::int64_t n, int c, const char* path) {
+    try {
+        write_trace_jsonl(path, make_trace(arrival, in_tok, out_tok, scores, n, c));
+        return ok(json(n), 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// read_trace_jsonl (domain.cpp:361-387) into caller-owned SoA buffers
+/// (capacity records, stage-major with stride n).  ok JSON {"n":..,"stages":..}.
+char* ref_read_trace_jsonl(const char* path, double* arrival, double* in_tok, double* out_tok,
+                           double* scores, std::int64_t capacity, int max_stages) {
+    try {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto trace = read_trace_jsonl(path);
+        const double el = seconds_since(t0);
+        const std::int64_t n = static_cast<std::int64_t>(trace.size());
+        const int c = n ? static_cast<int>(trace.front().per_stage.size()) : 0;
+        if (n > capacity || c > max_stages) throw std::runtime_error("capacity too small");
+        for (std::int64_t r = 0; r < n; ++r) {
+            arrival[r] = trace[r].arrival_s;
+            in_tok[r] = trace[r].input_tokens;
+            for (int i = 0; i < c; ++i) {
+                out_tok[static_cast<std::int64_t>(i) * n + r] = trace[r].per_stage[i].output_tokens;
+                scores[static_cast<std::int64_t>(i) * n + r] = trace[r].per_stage[i].score;
+            }
+        }
+        return ok(json{{"n", n}, {"stages", c}}, el);
     } catch (const CascadeError& e) {
         return fail(e);
     } catch (const std::exception& e) {

@@ -46,6 +46,8 @@ def lib():
             "ref_weight_ladder": [ctypes.c_double, ctypes.c_double, ctypes.c_int],
             "ref_pareto": [_D, _D, ctypes.c_int64],
             "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
+            "ref_write_trace_jsonl": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p],
+            "ref_read_trace_jsonl": [ctypes.c_char_p, _D, _D, _D, _D, ctypes.c_int64, ctypes.c_int],
         }.items():
             f = getattr(L, name)
             f.argtypes = args
@@ -160,3 +162,21 @@ def pareto(latency, quality) -> list:
 
 def max_threads() -> int:
     return int(lib().ref_max_threads())
+
+
+def write_trace_jsonl(trace: dict, path: str) -> None:
+    """The reference writer (nlohmann dump of each TraceRecord + '\\n')."""
+    keep, n, c = _trace_args(trace)
+    _unwrap(_call(lib().ref_write_trace_jsonl, *map(_ptr, keep), n, c, path.encode()))
+
+
+def read_trace_jsonl(path: str, capacity: int, max_stages: int = 16) -> dict:
+    """The reference reader; raises RefError with the reference's code/message."""
+    cap = max(1, capacity)
+    arr, inp = np.zeros(cap), np.zeros(cap)
+    out, sc = np.zeros(cap * max_stages), np.zeros(cap * max_stages)
+    res = _unwrap(_call(lib().ref_read_trace_jsonl, path.encode(), _ptr(arr), _ptr(inp), _ptr(out), _ptr(sc),
+                        capacity, max_stages))
+    n, c = res["result"]["n"], res["result"]["stages"]
+    return {"arrival_s": arr[:n], "input_tokens": inp[:n], "output_tokens": out[: n * c].reshape(c, n),
+            "scores": sc[: n * c].reshape(c, n), "elapsed_s": res["elapsed_s"]}

@@ -28,6 +28,7 @@
 
 #include "cascade_gpu.h"
 #include "cg_cuda.h"
+#include "cg_ingest.h"
 #include "cg_internal.h"
 #include "cg_kernels.h"
 #include "host_model.h"
@@ -154,6 +155,7 @@ struct cg_engine {
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc;
+    IngestBuffers ingest;
 };
 
 namespace {
@@ -836,6 +838,83 @@ void free_result(cg_sweep_result* r) {
 extern "C" {
 
 const char* cg_version(void) { return "cascade-gpu 0.1 (sm_100a)"; }
+
+void cg_trace_buffer_free(cg_trace_buffer* b) {
+    if (!b) return;
+    std::free(const_cast<double*>(b->host.arrival_s));
+    std::free(const_cast<double*>(b->host.input_tokens));
+    std::free(const_cast<double*>(b->host.output_tokens));
+    std::free(const_cast<double*>(b->host.scores));
+    delete b;
+}
+
+static cg_status ingest_common(cg_engine* E, const char* bytes, int64_t len, const std::string& path,
+                               double ms_read, cg_trace_buffer** out) {
+    return guarded([&] {
+        if (!E || !out || (len > 0 && !bytes)) fail(CG_ERR_INVALID_INPUT, "null engine/buffer");
+        *out = nullptr;
+        Timer tm;
+        IngestOut io;
+        ingest_jsonl(E->ingest, E->s, bytes, len, path, io);
+        auto* b = new cg_trace_buffer{};
+        const long long n = io.n;
+        const int C = io.stages;
+        auto alloc = [](size_t count) {
+            double* p = static_cast<double*>(std::malloc(std::max<size_t>(1, count) * sizeof(double)));
+            if (!p) throw std::bad_alloc();
+            return p;
+        };
+        double* ha = alloc(n);
+        double* hi = alloc(n);
+        double* ho = alloc((size_t)C * n);
+        double* hs = alloc((size_t)C * n);
+        b->host = cg_trace{n, C, 0, ha, hi, ho, hs};
+        b->device = cg_trace{n, C, 1, io.d_arrival, io.d_in, io.d_out, io.d_scores};
+        if (n > 0) {
+            CG_CUDA(cudaMemcpyAsync(ha, io.d_arrival, n * 8, cudaMemcpyDeviceToHost, E->s));
+            CG_CUDA(cudaMemcpyAsync(hi, io.d_in, n * 8, cudaMemcpyDeviceToHost, E->s));
+            if (C > 0) {
+                CG_CUDA(cudaMemcpyAsync(ho, io.d_out, (size_t)C * n * 8, cudaMemcpyDeviceToHost, E->s));
+                CG_CUDA(cudaMemcpyAsync(hs, io.d_scores, (size_t)C * n * 8, cudaMemcpyDeviceToHost, E->s));
+            }
+            CG_CUDA(cudaStreamSynchronize(E->s));
+        }
+        b->stats.bytes = len;
+        b->stats.lines = io.lines;
+        b->stats.records = n;
+        b->stats.host_lines = io.host_lines;
+        b->stats.gpu_launches = io.launches;
+        b->stats.ms_total = tm.ms();
+        b->stats.ms_read = ms_read;
+        *out = b;
+    });
+}
+
+cg_status cg_parse_trace_jsonl(cg_engine* E, const char* bytes, int64_t len, const char* path,
+                               cg_trace_buffer** out) {
+    return ingest_common(E, bytes, len, path ? path : "<memory>", 0.0, out);
+}
+
+cg_status cg_read_trace_jsonl(cg_engine* E, const char* path, cg_trace_buffer** out) {
+    if (!E || !path || !out) return err_status(CG_ERR_INVALID_INPUT, "null engine/path");
+    Timer tm;
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return err_status(CG_ERR_IO, std::string("cannot open trace file: ") + path);
+    long long len = 0;
+    char* buf = nullptr;
+    cg_status st = guarded([&] {
+        if (std::fseek(f, 0, SEEK_END) != 0) fail(CG_ERR_IO, std::string("cannot open trace file: ") + path);
+        len = std::ftell(f);
+        std::fseek(f, 0, SEEK_SET);
+        if (len < 0) fail(CG_ERR_IO, std::string("cannot open trace file: ") + path);
+        buf = static_cast<char*>(E->ingest.pinned.reserve((size_t)len + 1));
+        if (len > 0 && std::fread(buf, 1, (size_t)len, f) != (size_t)len)
+            fail(CG_ERR_IO, std::string("cannot open trace file: ") + path);
+    });
+    std::fclose(f);
+    if (st.code != CG_OK) return st;
+    return ingest_common(E, buf, len, path, tm.ms(), out);
+}
 
 cg_status cg_engine_create(int32_t device, cg_engine** out) {
     return guarded([&] {

@@ -8,6 +8,7 @@ Names, argument meaning and error behaviour follow the reference C++ API:
     StageEvaluator(hw, params).row(model, w, budget)   cascade::costmodel::StageEvaluator::row
     solve_min_max(table, total_gpus)                   cascade::innerplan::solve_min_max
     generate_trace(spec, seed)                         cascade::cli::generate_trace
+    read_trace_jsonl(path)                             cascade::read_trace_jsonl
 
 Results are returned in the reference's JSON schema (plain dicts, the
 structure nlohmann::json(SweepResult) produces), errors raise CascadeError
@@ -140,13 +141,24 @@ class RowResultC(ctypes.Structure):
                 ("replicas", ctypes.POINTER(Replica)), ("stats", SweepStats)]
 
 
+class IngestStats(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_int64), ("lines", ctypes.c_int64), ("records", ctypes.c_int64),
+                ("host_lines", ctypes.c_int64), ("gpu_launches", ctypes.c_int32), ("ms_total", ctypes.c_double),
+                ("ms_read", ctypes.c_double)]
+
+
+class TraceBufferC(ctypes.Structure):
+    _fields_ = [("host", Trace), ("device", Trace), ("stats", IngestStats)]
+
+
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                 ctypes.c_void_p)
 
 EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_engine_set_collective", "cg_engine_set_option",
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
             "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
-            "cg_merge_row_shards", "cg_shard_range"]
+            "cg_merge_row_shards", "cg_shard_range", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
+            "cg_trace_buffer_free"]
 
 _lib = None
 
@@ -201,6 +213,14 @@ def library():
                                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]
         L.cg_generate_trace.restype = Status
         L.cg_version.restype = ctypes.c_char_p
+        L.cg_read_trace_jsonl.argtypes = [ctypes.c_void_p, ctypes.c_char_p,
+                                          ctypes.POINTER(ctypes.POINTER(TraceBufferC))]
+        L.cg_read_trace_jsonl.restype = Status
+        L.cg_parse_trace_jsonl.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p,
+                                           ctypes.POINTER(ctypes.POINTER(TraceBufferC))]
+        L.cg_parse_trace_jsonl.restype = Status
+        L.cg_trace_buffer_free.argtypes = [ctypes.POINTER(TraceBufferC)]
+        L.cg_trace_buffer_free.restype = None
         L.cg_engine_stream.argtypes = [ctypes.c_void_p]
         L.cg_engine_stream.restype = ctypes.c_void_p
         _lib = L
@@ -411,6 +431,48 @@ class Engine:
         finally:
             self._lib.cg_sweep_result_free(out)
 
+    # -- cascade::read_trace_jsonl (trace ingest on the GPU)
+    def read_trace_jsonl(self, path: str) -> dict:
+        """SoA trace dict (arrival_s, input_tokens, output_tokens[C][n], scores[C][n])."""
+        out = ctypes.POINTER(TraceBufferC)()
+        _check(self._lib.cg_read_trace_jsonl(self._h, os.fsencode(path), ctypes.byref(out)))
+        return self._take_trace(out)
+
+    def ingest_to_device(self, path: str) -> "TraceBuffers":
+        """Ingest into HBM and return the device-resident columns (engine-owned,
+        valid until the next ingest on this engine) for sweep()/route_grid()."""
+        out = ctypes.POINTER(TraceBufferC)()
+        _check(self._lib.cg_read_trace_jsonl(self._h, os.fsencode(path), ctypes.byref(out)))
+        try:
+            b = out.contents
+            d = b.device
+            self.last_ingest = {name: getattr(b.stats, name) for name, _ in IngestStats._fields_}
+            return TraceBuffers(d.arrival_s, d.input_tokens, d.output_tokens, d.scores, on_device=True,
+                                keep={"n": int(d.n), "stages": int(d.stages)})
+        finally:
+            self._lib.cg_trace_buffer_free(out)
+
+    def parse_trace_jsonl(self, data: bytes, path: str = "<memory>") -> dict:
+        out = ctypes.POINTER(TraceBufferC)()
+        _check(self._lib.cg_parse_trace_jsonl(self._h, data, len(data), path.encode(), ctypes.byref(out)))
+        return self._take_trace(out)
+
+    def _take_trace(self, out) -> dict:
+        try:
+            b = out.contents
+            n, C = int(b.host.n), int(b.host.stages)
+
+            def col(ptr, count):
+                if count == 0:
+                    return np.zeros(0)
+                return np.ctypeslib.as_array(ctypes.cast(ptr, _DP), shape=(count,)).copy()
+            self.last_ingest = {name: getattr(b.stats, name) for name, _ in IngestStats._fields_}
+            return {"arrival_s": col(b.host.arrival_s, n), "input_tokens": col(b.host.input_tokens, n),
+                    "output_tokens": col(b.host.output_tokens, C * n).reshape(C, n),
+                    "scores": col(b.host.scores, C * n).reshape(C, n)}
+        finally:
+            self._lib.cg_trace_buffer_free(out)
+
     # -- cascade::routing::route_trace
     def route_trace(self, trace, thresholds: Sequence[float], deployed: Sequence[bool],
                     with_accept: bool = False) -> dict:
@@ -574,6 +636,10 @@ def sweep(trace, models, hw, params, total_gpus, cfg=None) -> dict:
 
 def route_trace(trace, thresholds, deployed) -> dict:
     return default_engine().route_trace(trace, thresholds, deployed)
+
+
+def read_trace_jsonl(path: str) -> dict:
+    return default_engine().read_trace_jsonl(path)
 
 
 def solve_min_max(table: dict, total_gpus: int) -> dict:
