@@ -19,6 +19,9 @@
  *                            include/cascade/cli.hpp:171-172, src/cli.cpp:428-460
  *   cg_read_trace_jsonl   <- cascade::read_trace_jsonl (trace ingest)
  *                            include/cascade/domain.hpp:162, src/domain.cpp:361-387
+ *   cg_sweep_result_json  <- nlohmann::json(SweepResult).dump(indent) / json(front).dump(indent)
+ *                            (sweep.json / front.json, src/cli.cpp:121,165-172,
+ *                            src/outerplan.cpp:20-59, src/domain.cpp:270-356)
  *
  * Conventions
  *   - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
@@ -322,6 +325,18 @@ cg_status cg_read_trace_jsonl(cg_engine* engine, const char* path, cg_trace_buff
 cg_status cg_parse_trace_jsonl(cg_engine* engine, const char* bytes, int64_t len, const char* path,
                                cg_trace_buffer** out);
 void cg_trace_buffer_free(cg_trace_buffer* buffer);
+
+/* Output serialisation: the exact bytes nlohmann's dump(indent) writes for
+ * json(SweepResult) (what = 0, sweep.json without its trailing "\n") or
+ * json(SweepResult::front) (what = 1, front.json), formatted on the GPU.
+ * flags: CG_JSON_COMPACT_INT_ARRAYS reproduces nlohmann builds that print
+ * integer arrays on one line (the cudnn-frontend copy of 3.11.3 in this image
+ * does; upstream 3.11.3 does not -- bindings probe their own nlohmann once).
+ * *text is NUL-terminated, owned by the caller (cg_text_free). */
+#define CG_JSON_COMPACT_INT_ARRAYS 1
+cg_status cg_sweep_result_json(cg_engine* engine, const cg_sweep_result* result, int32_t indent, int32_t what,
+                               int32_t flags, char** text, int64_t* len);
+void cg_text_free(char* text);
 
 const char* cg_version(void);
 

@@ -18,6 +18,7 @@
 
 #include "cascade/cli.hpp"
 #include "cascade/outerplan.hpp"
+#include "output_gpu.hpp"
 
 namespace cascade {
 std::vector<TraceRecord> cpu_read_trace_jsonl(const std::string& path);
@@ -84,6 +85,22 @@ int main(int argc, char** argv) {
     cli::write_output_file(out + "/cpu", "front.csv", outerplan::front_to_csv(res.front));
     cli::write_output_file(out + "/cpu", "sweep.json", json(res).dump(2) + "\n");
 
+    // GPU output writer vs the reference's nlohmann dump of the same result
+    t0 = std::chrono::steady_clock::now();
+    const std::string cpu_sweep_text = json(res).dump(2) + "\n";
+    const double cpu_dump_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    t0 = std::chrono::steady_clock::now();
+    const std::string gpu_sweep_text = outerplan::sweep_json(res, 2) + "\n";
+    const std::string gpu_front_text = outerplan::front_json(res, 2) + "\n";
+    const double gpu_dump_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const bool writer_identical = gpu_sweep_text == cpu_sweep_text &&
+                                  gpu_front_text == json(res.front).dump(2) + "\n";
+
+    if (!writer_identical) {  // keep both texts for inspection
+        cli::write_output_file(out, "writer_gpu_sweep.json", gpu_sweep_text);
+        cli::write_output_file(out, "writer_ref_sweep.json", cpu_sweep_text);
+    }
+
     json report;
     bool all = true;
     for (const char* f : {"plan.json", "front.json", "front.csv", "sweep.json"}) {
@@ -91,7 +108,10 @@ int main(int argc, char** argv) {
         report["files"][f] = {{"identical", a == b}, {"bytes", a.size()}};
         all = all && a == b;
     }
-    all = all && trace_identical;
+    all = all && trace_identical && writer_identical;
+    report["writer_identical"] = writer_identical;
+    report["cpu_dump_s"] = cpu_dump_s;
+    report["gpu_dump_s"] = gpu_dump_s;
     report["trace_identical"] = trace_identical;
     report["gpu_read_s"] = gpu_read_s;
     report["cpu_read_s"] = cpu_read_s;

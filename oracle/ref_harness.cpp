@@ -261,6 +261,33 @@ char* ref_generate_trace(const char* spec_json, std::uint64_t seed, double* arri
     }
 }
 
+/// cmd_plan's sweep.json / front.json payloads (cli.cpp:121,167-172) of a
+/// SweepResult given as JSON: from_json, then json(res).dump(2) timed.
+char* ref_dump_sweep(const char* sweep_json) {
+    try {
+        const json j = json::parse(sweep_json);
+        outerplan::SweepResult res;  // no from_json(SweepResult) in the reference: member-wise
+        j.at("front").get_to(res.front);
+        j.at("evaluations").get_to(res.evaluations);
+        j.at("weights").get_to(res.weights);
+        j.at("weight_selection").get_to(res.weight_selection);
+        j.at("utopia").get_to(res.utopia);
+        j.at("skipped").get_to(res.skipped);
+        const auto t0 = std::chrono::steady_clock::now();
+        std::string sweep_text = json(res).dump(2) + "\n";
+        std::string front_text = json(res.front).dump(2) + "\n";
+        const double el = seconds_since(t0);
+        json files;
+        files["sweep.json"] = std::move(sweep_text);
+        files["front.json"] = std::move(front_text);
+        return ok(files, el);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
 /// write_trace_jsonl (domain.cpp:389-394) of SoA columns.
 char* ref_write_trace_jsonl(const double* arrival, const double* in_tok, const double* out_tok,
                             const double* scores, std::int64_t n, int c, const char* path) {

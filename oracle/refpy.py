@@ -46,6 +46,7 @@ def lib():
             "ref_weight_ladder": [ctypes.c_double, ctypes.c_double, ctypes.c_int],
             "ref_pareto": [_D, _D, ctypes.c_int64],
             "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
+            "ref_dump_sweep": [ctypes.c_char_p],
             "ref_write_trace_jsonl": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p],
             "ref_read_trace_jsonl": [ctypes.c_char_p, _D, _D, _D, _D, ctypes.c_int64, ctypes.c_int],
         }.items():
@@ -180,3 +181,12 @@ def read_trace_jsonl(path: str, capacity: int, max_stages: int = 16) -> dict:
     n, c = res["result"]["n"], res["result"]["stages"]
     return {"arrival_s": arr[:n], "input_tokens": inp[:n], "output_tokens": out[: n * c].reshape(c, n),
             "scores": sc[: n * c].reshape(c, n), "elapsed_s": res["elapsed_s"]}
+
+
+def dump_sweep(result: dict) -> dict:
+    """The reference's sweep.json / front.json text of a SweepResult (JSON dict),
+    plus the time json(res).dump(2) took ("elapsed_s")."""
+    res = _unwrap(_call(lib().ref_dump_sweep, json.dumps(result).encode()))
+    out = dict(res["result"])
+    out["elapsed_s"] = res["elapsed_s"]
+    return out

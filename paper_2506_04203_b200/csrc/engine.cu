@@ -29,6 +29,7 @@
 #include "cascade_gpu.h"
 #include "cg_cuda.h"
 #include "cg_ingest.h"
+#include "cg_json.h"
 #include "cg_internal.h"
 #include "cg_kernels.h"
 #include "host_model.h"
@@ -156,6 +157,7 @@ struct cg_engine {
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc;
     IngestBuffers ingest;
+    JsonBuffers jsonbuf;
 };
 
 namespace {
@@ -838,6 +840,27 @@ void free_result(cg_sweep_result* r) {
 extern "C" {
 
 const char* cg_version(void) { return "cascade-gpu 0.1 (sm_100a)"; }
+
+cg_status cg_sweep_result_json(cg_engine* E, const cg_sweep_result* r, int32_t indent, int32_t what,
+                               int32_t flags, char** text, int64_t* len) {
+    return guarded([&] {
+        if (!E || !r || !text || !len) fail(CG_ERR_INVALID_INPUT, "null engine/result/output");
+        if (indent < 0) fail(CG_ERR_UNSUPPORTED, "compact JSON (indent < 0) is not produced by the planner");
+        if (what != 0 && what != 1) fail(CG_ERR_INVALID_INPUT, "what must be 0 (sweep) or 1 (front)");
+        *text = nullptr;
+        *len = 0;
+        int launches = 0;
+        const std::string s = result_json(E->jsonbuf, E->s, *r, indent, what, flags, &launches);
+        char* p = static_cast<char*>(std::malloc(s.size() + 1));
+        if (!p) throw std::bad_alloc();
+        std::memcpy(p, s.data(), s.size());
+        p[s.size()] = 0;
+        *text = p;
+        *len = (int64_t)s.size();
+    });
+}
+
+void cg_text_free(char* text) { std::free(text); }
 
 void cg_trace_buffer_free(cg_trace_buffer* b) {
     if (!b) return;

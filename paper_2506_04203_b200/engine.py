@@ -141,6 +141,11 @@ class RowResultC(ctypes.Structure):
                 ("replicas", ctypes.POINTER(Replica)), ("stats", SweepStats)]
 
 
+# The reference's JSON files are written by its nlohmann build; the one in this
+# image (and therefore the compiled oracle) prints integer arrays on one line.
+JSON_FLAGS = int(os.environ.get("CASCADE_JSON_FLAGS", "1"))
+
+
 class IngestStats(ctypes.Structure):
     _fields_ = [("bytes", ctypes.c_int64), ("lines", ctypes.c_int64), ("records", ctypes.c_int64),
                 ("host_lines", ctypes.c_int64), ("gpu_launches", ctypes.c_int32), ("ms_total", ctypes.c_double),
@@ -158,7 +163,7 @@ EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_eng
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
             "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
             "cg_merge_row_shards", "cg_shard_range", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
-            "cg_trace_buffer_free"]
+            "cg_trace_buffer_free", "cg_sweep_result_json", "cg_text_free"]
 
 _lib = None
 
@@ -219,6 +224,12 @@ def library():
         L.cg_parse_trace_jsonl.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p,
                                            ctypes.POINTER(ctypes.POINTER(TraceBufferC))]
         L.cg_parse_trace_jsonl.restype = Status
+        L.cg_sweep_result_json.argtypes = [ctypes.c_void_p, ctypes.POINTER(SweepResultC), ctypes.c_int32,
+                                           ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p),
+                                           ctypes.POINTER(ctypes.c_int64)]
+        L.cg_sweep_result_json.restype = Status
+        L.cg_text_free.argtypes = [ctypes.c_void_p]
+        L.cg_text_free.restype = None
         L.cg_trace_buffer_free.argtypes = [ctypes.POINTER(TraceBufferC)]
         L.cg_trace_buffer_free.restype = None
         L.cg_engine_stream.argtypes = [ctypes.c_void_p]
@@ -411,7 +422,9 @@ class Engine:
 
     # -- cascade::outerplan::sweep
     def sweep(self, trace, models, hw: dict, params: Optional[dict], total_gpus: int,
-              cfg: Optional[dict] = None, raw: bool = False):
+              cfg: Optional[dict] = None, raw: bool = False, files: bool = False):
+        """files=True also renders sweep.json / front.json on the GPU exactly as
+        cmd_plan writes them (dump(2) + "\\n") into self.last_files."""
         tb = _as_trace(trace)
         tc = tb.c()
         marr, keep = models_c(models)
@@ -425,11 +438,24 @@ class Engine:
         try:
             r = out.contents
             self.last_stats = _stats_dict(r.stats)
+            if files:
+                self.last_files = {"sweep.json": self._result_text(out, 2, 0) + "\n",
+                                   "front.json": self._result_text(out, 2, 1) + "\n"}
             if raw:
                 return None
             return _sweep_to_json(r)
         finally:
             self._lib.cg_sweep_result_free(out)
+
+    def _result_text(self, res_ptr, indent: int, what: int) -> str:
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        _check(self._lib.cg_sweep_result_json(self._h, res_ptr, int(indent), int(what), JSON_FLAGS,
+                                              ctypes.byref(p), ctypes.byref(n)))
+        try:
+            return ctypes.string_at(p, n.value).decode()
+        finally:
+            self._lib.cg_text_free(p)
 
     # -- cascade::read_trace_jsonl (trace ingest on the GPU)
     def read_trace_jsonl(self, path: str) -> dict:
