@@ -51,8 +51,9 @@ struct RowTables {
     double* prefill;
     double* decode;
     double* mean_service;
-    double* T;            // [row][n_req] CRN arrivals
-    double* O;            // [row][n_req] CRN outputs
+    double* T;            // [row][ld] CRN arrivals (first n_req used)
+    double* O;            // [row][ld] CRN outputs
+    int ld;               // row stride: n_req rounded up to a multiple of 4 (32-byte rows)
 };
 
 struct SimItem {

@@ -142,6 +142,8 @@ struct cg_engine {
     cg_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
     int prune = 1;
+    int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
+    std::vector<unsigned long long> ub_saved;
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
@@ -245,8 +247,11 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     tab.prefill = E.d_pre.as<double>((size_t)nrows * kMaxShapes);
     tab.decode = E.d_dec.as<double>((size_t)nrows * kMaxShapes);
     tab.mean_service = E.d_ms.as<double>((size_t)nrows * kMaxShapes);
-    tab.T = E.d_T.as<double>((size_t)nrows * n_req);
-    tab.O = E.d_O.as<double>((size_t)nrows * n_req);
+    tab.ld = (n_req + 3) & ~3;
+    tab.T = E.d_T.as<double>((size_t)nrows * tab.ld);
+    tab.O = E.d_O.as<double>((size_t)nrows * tab.ld);
+    CG_CUDA(cudaMemsetAsync(tab.T, 0, (size_t)nrows * tab.ld * 8, x.s));
+    CG_CUDA(cudaMemsetAsync(tab.O, 0, (size_t)nrows * tab.ld * 8, x.s));
     {
         auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
         double* dL = E.d_crn.as<double>(L.size());
@@ -268,6 +273,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     unsigned long long* ub = E.d_ub.as<unsigned long long>(cells);
     x.fill(latmin, cells, kInfBits);
     x.fill(ub, cells, kInfBits);
+    if (E.ub_oracle && E.ub_saved.size() == (size_t)cells)
+        x.h2d(ub, E.ub_saved.data(), (size_t)cells * 8);  // diagnostic: the exact final bounds
     TieEntry* ties = E.d_ties.as<TieEntry>(E.tie_cap);
     unsigned long long* tiecnt = E.d_tiecnt.as<unsigned long long>(1);
     unsigned long long* ovf = E.d_ovf.as<unsigned long long>(E.ovf_cap);
@@ -490,6 +497,11 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         ra.nties = 0;
     }
     launch_resolve(ra, x.s, &x.launches);
+    if (E.ub_oracle) {
+        E.ub_saved.resize((size_t)cells);
+        x.d2h(E.ub_saved.data(), ra.final_lat, (size_t)cells * 8);
+        x.sync();
+    }
 }
 
 // ParallelismPlan expansion of plan index p in space sp (canonical order).
@@ -987,6 +999,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         const std::string k(key);
         if (k == "prune") e->prune = value ? 1 : 0;
         else if (k == "k1_form") e->k1_form = (int)value;
+        else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);

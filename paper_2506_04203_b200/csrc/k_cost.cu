@@ -105,8 +105,8 @@ __global__ void k_row_crn(RowSetupArgs a, const double* __restrict__ L) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= a.nrows) return;
     const RowDesc rd = a.rows[row];
-    double* T = a.tab.T + (long long)row * a.n_req;
-    double* O = a.tab.O + (long long)row * a.n_req;
+    double* T = a.tab.T + (long long)row * a.tab.ld;
+    double* O = a.tab.O + (long long)row * a.tab.ld;
     const double cap = __dmul_rn(4.0, rd.mean_out);
     const double neg_mean = -rd.mean_out;
     double t = 0.0;
@@ -161,8 +161,8 @@ __device__ __forceinline__ void count_add(unsigned long long* ctr, unsigned long
 __device__ __forceinline__ double service_bound(const SimArgs& a, int row, const PlanSpace& sp,
                                                 const unsigned char* counts) {
     const long long rb = (long long)row * kMaxShapes;
-    const double o_k = a.tab.O[(long long)row * a.n_req + a.kstar];
-    const double t_max = a.tab.T[(long long)row * a.n_req + a.n_req - 1];
+    const double o_k = a.tab.O[(long long)row * a.tab.ld + a.kstar];
+    const double t_max = a.tab.T[(long long)row * a.tab.ld + a.n_req - 1];
     double lb = __longlong_as_double(0x7ff0000000000000ll);
     for (int s = 0; s < sp.S; ++s) {
         if (!counts[s]) continue;
@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
     if (gl == 0) gs.status = ST_NEED;
     __syncwarp();
 
+    const int n_req = a.n_req;
     int status = ST_NEED;
     int row = 0, dp = 0, gpus = 0, k = 0, ab = 0;
     unsigned long long plan = 0;
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                     gpus = gs.used;
                     plan = gs.plan;
                     const PlanSpace& sp = a.spaces[a.rows[row].space];
-                    Trow = a.tab.T + (long long)row * a.n_req;
-                    Orow = a.tab.O + (long long)row * a.n_req;
+                    Trow = a.tab.T + (long long)row * a.tab.ld;
+                    Orow = a.tab.O + (long long)row * a.tab.ld;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = r * W + gl;
@@ -393,78 +394,106 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
 
-        // ---- phase B: UNROLL JSQ dispatch steps per running group.  The
-        // winner's update is predicated (no divergent branch); only the rare
-        // all-busy case takes the butterfly-min path.
+        // ---- phase B: UNROLL JSQ dispatch steps per running group.
+        // k is a multiple of UNROLL here (plans start at k = 0 and advance
+        // UNROLL per trip), so the next arrivals/outputs come in with vector
+        // loads.  A replica is idle at t iff its last finish time avail <= t
+        // (FCFS: every job it holds is done by then), so the common case --
+        // some replica idle -- needs no queue bookkeeping at all: the winner
+        // is the lowest idle index (the reference's early break), its start
+        // is t and its FIFO is reset to the new job.  Only when every replica
+        // of a group is busy are the FIFOs popped up to t (lazily -- pops are
+        // idempotent in t) and the winner taken as the group minimum of
+        // (queue length << 9 | replica index), the reference's argmin.
+        {
+            const bool run0 = status == ST_RUN;
+            const double2* T2 = reinterpret_cast<const double2*>(Trow + (run0 ? k : 0));
+            const double2* O2 = reinterpret_cast<const double2*>(Orow + (run0 ? k : 0));
+            const double2 ta = __ldg(T2), tb = __ldg(T2 + 1), oa = __ldg(O2), ob = __ldg(O2 + 1);
+            const double tt[4] = {ta.x, ta.y, tb.x, tb.y};
+            const double oo[4] = {oa.x, oa.y, ob.x, ob.y};
+            double* const srow = scratch + k;
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const bool run = status == ST_RUN;
-            const int kk = run ? k : 0;
-            const double t = __ldg(&Trow[kk]);
-            const double o = __ldg(&Orow[kk]);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                while (run && nd[r] <= t) {  // departures up to t (fin <= t has left)
-                    --cnt[r];
-                    if (cnt[r] > 0) {
-                        const int slotr = head[r] & ring_mask;
-                        nd[r] = DEEP ? gring[((long long)r * ring_cap + slotr) * 32 + lane]
-                                     : ring[(r * CAP + slotr) * 32 + lane];
-                        ++head[r];
-                    } else {
-                        nd[r] = INF;
-                    }
-                }
-            }
-            int win = -1;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const bool idle = run && cnt[r] == 0 && (r * W + gl) < dp;
-                const unsigned gb = (__ballot_sync(FULL, idle) >> gshift) & wmask;
-                if (win < 0 && gb) win = r * W + (__ffs(gb) - 1);
-            }
-            const bool all_busy = run && win < 0;
-            if (__any_sync(FULL, all_busy)) {
-                unsigned key = 0xffffffffu;
+            for (int u = 0; u < UNROLL; ++u) {
+                const bool run = status == ST_RUN;
+                const double t = tt[u];
+                const double o = oo[u];
+                // fast path: lowest idle replica of the group
+                int win = -1;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const int j = r * W + gl;
-                    if (j < dp) {
-                        const unsigned kk2 = ((unsigned)cnt[r] << 9) | (unsigned)j;
-                        key = kk2 < key ? kk2 : key;
+                    const bool idle = run && (r * W + gl) < dp && avail[r] <= t;
+                    const unsigned gb = (__ballot_sync(FULL, idle) >> gshift) & wmask;
+                    if (win < 0 && gb) win = r * W + (__ffs(gb) - 1);
+                }
+                const bool busy = run && win < 0;
+                if (__any_sync(FULL, busy)) {
+                    // slow path (groups whose replicas are all busy): pop the
+                    // FIFOs up to t, then the (length, index) group minimum
+                    bool dep[R];
+                    bool anydep = false;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        dep[r] = busy && nd[r] <= t;
+                        anydep |= dep[r];
+                    }
+                    while (__any_sync(FULL, anydep)) {
+                        anydep = false;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const int slotr = head[r] & ring_mask;
+                            const double nx = DEEP ? gring[((long long)r * ring_cap + slotr) * 32 + lane]
+                                                   : ring[(r * CAP + slotr) * 32 + lane];
+                            const int c1 = cnt[r] - (dep[r] ? 1 : 0);
+                            nd[r] = dep[r] ? (c1 > 0 ? nx : INF) : nd[r];
+                            head[r] += (dep[r] && c1 > 0) ? 1 : 0;
+                            cnt[r] = c1;
+                            dep[r] = busy && nd[r] <= t;
+                            anydep |= dep[r];
+                        }
+                    }
+                    unsigned key = 0xffffffffu;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int j = r * W + gl;
+                        const unsigned kr = ((unsigned)cnt[r] << 9) | (unsigned)j;
+                        key = (busy && j < dp && kr < key) ? kr : key;
+                    }
+#pragma unroll
+                    for (int off = W / 2; off > 0; off >>= 1) {
+                        const unsigned v = __shfl_xor_sync(FULL, key, off);
+                        key = v < key ? v : key;
+                    }
+                    if (busy) win = (int)(key & 511u);
+                }
+                const int wl = win & (W - 1), wr = win / W;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool me = run && gl == wl && r == wr;
+                    const bool was_idle = avail[r] <= t;
+                    const double start = was_idle ? t : avail[r];  // std::max(t, avail)
+                    const double fin = __dadd_rn(__dadd_rn(start, pre[r]), __dmul_rn(o, dec[r]));
+                    const double soj = __dsub_rn(fin, t);
+                    if (me) {
+                        if (was_idle) {  // empty FIFO: the new job is in service
+                            head[r] = tail[r];
+                            cnt[r] = 1;
+                            nd[r] = fin;
+                        } else {         // joins the queue behind the busy server
+                            const int slotr = tail[r] & ring_mask;
+                            if (DEEP) gring[((long long)r * ring_cap + slotr) * 32 + lane] = fin;
+                            else ring[(r * CAP + slotr) * 32 + lane] = fin;
+                            ++tail[r];
+                            ovf |= (tail[r] - head[r] > ring_cap);
+                            ++cnt[r];
+                        }
+                        avail[r] = fin;
+                        srow[u] = soj;
+                        ab += soj > U ? 1 : 0;
                     }
                 }
-#pragma unroll
-                for (int off = W / 2; off > 0; off >>= 1) {
-                    const unsigned v = __shfl_xor_sync(FULL, key, off);
-                    key = v < key ? v : key;
-                }
-                if (all_busy) win = (int)(key & 511u);
-            }
-            const int wl = win & (W - 1), wr = win / W;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const bool me = run && gl == wl && r == wr;
-                const double start = (t < avail[r]) ? avail[r] : t;  // std::max(t, avail)
-                const double fin = __dadd_rn(__dadd_rn(start, pre[r]), __dmul_rn(o, dec[r]));
-                const double soj = __dsub_rn(fin, t);
-                const bool push = me && cnt[r] > 0;
-                if (push) {
-                    const int slotr = tail[r] & ring_mask;
-                    if (DEEP) gring[((long long)r * ring_cap + slotr) * 32 + lane] = fin;
-                    else ring[(r * CAP + slotr) * 32 + lane] = fin;
-                }
-                if (me && cnt[r] == 0) nd[r] = fin;
-                tail[r] += push ? 1 : 0;
-                ovf |= push && (tail[r] - head[r] > ring_cap);
-                cnt[r] += me ? 1 : 0;
-                avail[r] = me ? fin : avail[r];
-                if (me) scratch[kk] = soj;
-                ab += (me && soj > U) ? 1 : 0;
-            }
-            if (run) {
-                ++k;
-                if (k == a.n_req) status = ST_FINISH;
+                k += run ? 1 : 0;
+                status = (run && k == n_req) ? ST_FINISH : status;
             }
         }
 
@@ -637,8 +666,8 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
         used = unrank_plan(sp, lo, c);
         for (int s = 0; s < sp.S; ++s) dp += c[s];
     }
-    const double o_k = active ? a.tab.O[(long long)row * a.n_req + a.kstar] : 0.0;
-    const double t_max = active ? a.tab.T[(long long)row * a.n_req + a.n_req - 1] : 0.0;
+    const double o_k = active ? a.tab.O[(long long)row * a.tab.ld + a.kstar] : 0.0;
+    const double t_max = active ? a.tab.T[(long long)row * a.tab.ld + a.n_req - 1] : 0.0;
     unsigned long long stable = 0, skipped = 0;
     const unsigned long long trips = a.chunk;
     for (unsigned long long k = 0; k < trips; ++k) {
