@@ -19,6 +19,8 @@
  *                            include/cascade/cli.hpp:171-172, src/cli.cpp:428-460
  *   cg_read_trace_jsonl   <- cascade::read_trace_jsonl (trace ingest)
  *                            include/cascade/domain.hpp:162, src/domain.cpp:361-387
+ *   cg_simulate           <- cascade::sim::run / sim::compare (validation simulator)
+ *                            include/cascade/simulator.hpp:69-88, src/simulator.cpp:177-334
  *   cg_sweep_result_json  <- nlohmann::json(SweepResult).dump(indent) / json(front).dump(indent)
  *                            (sweep.json / front.json, src/cli.cpp:121,165-172,
  *                            src/outerplan.cpp:20-59, src/domain.cpp:270-356)
@@ -337,6 +339,56 @@ void cg_trace_buffer_free(cg_trace_buffer* buffer);
 cg_status cg_sweep_result_json(cg_engine* engine, const cg_sweep_result* result, int32_t indent, int32_t what,
                                int32_t flags, char** text, int64_t* len);
 void cg_text_free(char* text);
+
+/* Validation simulator: sim::run (simulator.cpp:177-299) of every plan, or
+ * sim::compare (simulator.cpp:318-334, >= 2 plans, the first plan's dry-run
+ * SLO base shared) when compare != 0.  Same preconditions, Errc and messages
+ * as the reference ("run: invalid plan: ...;" from validate_plan, ...). */
+typedef struct cg_sim_config {      /* sim::SimConfig (simulator.hpp:20-28) */
+    uint64_t seed;
+    double slo_base_s;              /* <= 0: no-contention dry-run base */
+    const double* slo_scales;
+    int32_t num_scales;             /* <= 32 */
+    double warmup_fraction;
+} cg_sim_config;
+
+typedef struct cg_cascade_plan {    /* cascade::CascadePlan (domain.hpp:105-114) */
+    const int32_t* allocations;     /* [C] */
+    const double* processing_ratios;/* [C] */
+    const double* thresholds;       /* [C-1] */
+    const int32_t* has_plan;        /* [C] */
+    const int32_t* gpus_used;       /* [C] */
+    const int32_t* dp;              /* [C] replicas of each deployed stage */
+    const cg_replica* replicas;     /* concatenated, stage order */
+} cg_cascade_plan;
+
+typedef struct cg_sim_report {      /* sim::SimReport (simulator.hpp:40-48) */
+    double* end_to_end_s;           /* [n] trace order */
+    int32_t* accept_stage;          /* [n] 1-based */
+    double p95_s;
+    double throughput_rps;
+    int32_t num_scales;
+    double* attainment_scale;       /* [num_scales] */
+    double* attainment_fraction;    /* [num_scales] */
+    int32_t has_min_scale_95;
+    double min_scale_95;
+    double slo_base_s;
+    int32_t num_unstable;
+    int32_t unstable_stages[8];     /* 1-based */
+} cg_sim_report;
+
+typedef struct cg_sim_result {
+    int64_t n;
+    int32_t num_reports;
+    cg_sim_report* reports;
+    int32_t gpu_launches;
+    double ms_total;
+} cg_sim_result;
+
+cg_status cg_simulate(cg_engine* engine, const cg_trace* trace, const cg_model* models, int32_t num_models,
+                      const cg_hardware* hw, const cg_cost_params* params, const cg_sim_config* cfg,
+                      const cg_cascade_plan* plans, int32_t num_plans, int32_t compare, cg_sim_result** out);
+void cg_sim_result_free(cg_sim_result* result);
 
 const char* cg_version(void);
 

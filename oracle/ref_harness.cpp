@@ -30,6 +30,7 @@
 #include "cascade/innerplan.hpp"
 #include "cascade/outerplan.hpp"
 #include "cascade/routing.hpp"
+#include "cascade/simulator.hpp"
 #include "cascade/util.hpp"
 
 using nlohmann::json;
@@ -281,6 +282,32 @@ char* ref_dump_sweep(const char* sweep_json) {
         files["sweep.json"] = std::move(sweep_text);
         files["front.json"] = std::move(front_text);
         return ok(files, el);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// sim::run of one plan (compare == 0, plans_json = [plan]) or sim::compare
+/// of a plan list: json(SimReport) / json(CompareResult) (simulator.cpp).
+char* ref_simulate(const double* arrival, const double* in_tok, const double* out_tok,
+                   const double* scores, std::int64_t n, int c, const char* config_json,
+                   const char* plans_json, const char* sim_json, int compare) {
+    try {
+        auto cfg = json::parse(config_json).get<cli::PlannerConfig>();
+        std::vector<CascadePlan> plans;
+        for (const auto& p : json::parse(plans_json)) plans.push_back(p.get<CascadePlan>());
+        auto sc = json::parse(sim_json).get<sim::SimConfig>();
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        const auto t0 = std::chrono::steady_clock::now();
+        json out;
+        if (compare) {
+            out = sim::compare(plans, trace, cfg.models, cfg.hardware, cfg.cost_model, sc);
+        } else {
+            out = sim::run(plans.at(0), trace, cfg.models, cfg.hardware, cfg.cost_model, sc);
+        }
+        return ok(std::move(out), seconds_since(t0));
     } catch (const CascadeError& e) {
         return fail(e);
     } catch (const std::exception& e) {

@@ -47,6 +47,8 @@ def lib():
             "ref_pareto": [_D, _D, ctypes.c_int64],
             "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
             "ref_dump_sweep": [ctypes.c_char_p],
+            "ref_simulate": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
+                             ctypes.c_char_p, ctypes.c_int],
             "ref_write_trace_jsonl": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p],
             "ref_read_trace_jsonl": [ctypes.c_char_p, _D, _D, _D, _D, ctypes.c_int64, ctypes.c_int],
         }.items():
@@ -190,3 +192,10 @@ def dump_sweep(result: dict) -> dict:
     out = dict(res["result"])
     out["elapsed_s"] = res["elapsed_s"]
     return out
+
+
+def simulate(trace: dict, config: dict, plans: list, sim_cfg: dict, compare: bool = False) -> dict:
+    """sim::run(plans[0]) or sim::compare(plans): {"result": json(report), "elapsed_s": t}."""
+    keep, n, c = _trace_args(trace)
+    return _unwrap(_call(lib().ref_simulate, *map(_ptr, keep), n, c, json.dumps(config).encode(),
+                         json.dumps(plans).encode(), json.dumps(sim_cfg).encode(), 1 if compare else 0))

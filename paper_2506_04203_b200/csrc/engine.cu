@@ -30,6 +30,7 @@
 #include "cg_cuda.h"
 #include "cg_ingest.h"
 #include "cg_json.h"
+#include "cg_simrun.h"
 #include "cg_internal.h"
 #include "cg_kernels.h"
 #include "host_model.h"
@@ -160,6 +161,7 @@ struct cg_engine {
         d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
+    SimRunBuffers simbuf;
 };
 
 namespace {
@@ -873,6 +875,174 @@ cg_status cg_sweep_result_json(cg_engine* E, const cg_sweep_result* r, int32_t i
 }
 
 void cg_text_free(char* text) { std::free(text); }
+
+void cg_sim_result_free(cg_sim_result* r) {
+    if (!r) return;
+    for (int i = 0; i < r->num_reports; ++i) {
+        std::free(r->reports[i].end_to_end_s);
+        std::free(r->reports[i].accept_stage);
+        std::free(r->reports[i].attainment_scale);
+        std::free(r->reports[i].attainment_fraction);
+    }
+    std::free(r->reports);
+    delete r;
+}
+
+cg_status cg_simulate(cg_engine* E, const cg_trace* tr, const cg_model* models, int32_t C, const cg_hardware* hw,
+                      const cg_cost_params* q, const cg_sim_config* cfg, const cg_cascade_plan* plans,
+                      int32_t P, int32_t compare, cg_sim_result** out) {
+    return guarded([&] {
+        if (!E || !tr || !models || !hw || !q || !cfg || (P > 0 && !plans) || !out)
+            fail(CG_ERR_INVALID_INPUT, "null argument");
+        *out = nullptr;
+        Timer tm;
+        if (compare && P < 2) fail(CG_ERR_INVALID_INPUT, "compare requires >= 2 plans");
+        if (C < 1 || C > kSimMaxStages) fail(CG_ERR_UNSUPPORTED, "simulator supports 1..8 cascade stages");
+        if (cfg->num_scales < 0 || cfg->num_scales > 32) fail(CG_ERR_UNSUPPORTED, "at most 32 SLO scales");
+        const long long n = tr->n;
+        // run() preconditions per plan, in plan order (simulator.cpp:180-206)
+        std::vector<SimPlanDesc> desc(P);
+        std::vector<double> ppt, pfix, dpt;
+        for (int pi = 0; pi < P; ++pi) {
+            const cg_cascade_plan& p = plans[pi];
+            if (n <= 0) fail(CG_ERR_EMPTY_TRACE, "run: empty trace");
+            const auto probs = validate_cascade_plan(p, *hw, models, C);
+            if (!probs.empty()) {
+                std::string m = "run: invalid plan:";
+                for (const auto& x : probs) m += " " + x + ";";
+                fail(CG_ERR_INVALID_INPUT, m);
+            }
+            if (!(cfg->warmup_fraction >= 0.0 && cfg->warmup_fraction < 1.0))
+                fail(CG_ERR_INVALID_INPUT, "warmup_fraction outside [0,1)");
+            for (int k = 1; k < cfg->num_scales; ++k)
+                if (cfg->slo_scales[k] <= cfg->slo_scales[k - 1])
+                    fail(CG_ERR_INVALID_INPUT, "slo_scales must be sorted ascending");
+            for (int k = 0; k < cfg->num_scales; ++k)
+                if (cfg->slo_scales[k] <= 0) fail(CG_ERR_INVALID_INPUT, "slo_scales must be positive");
+            if (tr->stages != C) fail(CG_ERR_INVALID_INPUT, "trace record stage count != C");
+            SimPlanDesc& d = desc[pi];
+            d = SimPlanDesc{};
+            d.C = C;
+            d.entry = -1;
+            d.last = -1;
+            long long off = 0;
+            int nchain = 0;
+            for (int i = 0; i < kSimMaxStages; ++i) {
+                d.next[i] = -1;
+                d.chain[i] = -1;
+            }
+            for (int i = 0; i < C; ++i) {
+                const int dp = p.has_plan[i] ? p.dp[i] : 0;
+                d.dp[i] = dp;
+                d.roff[i] = (int)ppt.size();
+                d.thr[i] = i + 1 < C ? p.thresholds[i] : 0.0;
+                if (dp > 256) fail(CG_ERR_UNSUPPORTED, "simulator supports up to 256 replicas per stage");
+                for (int k = 0; k < dp; ++k) {  // build_context (simulator.cpp:123-143)
+                    const cg_replica& r = p.replicas[off + k];
+                    const double bubble = 1.0 + q->pipeline_bubble_factor * (r.pp - 1);
+                    ppt.push_back(2.0 * models[i].param_count /
+                                  (r.tp * r.pp * hw->flops_per_gpu * q->prefill_efficiency) * bubble);
+                    pfix.push_back(r.pp * q->comm_overhead_per_stage * bubble);
+                    dpt.push_back(models[i].param_count * models[i].bytes_per_param /
+                                      (r.tp * hw->mem_bandwidth_per_gpu * q->decode_bw_efficiency) +
+                                  r.pp * q->comm_overhead_per_stage);
+                }
+                off += dp;
+                if (dp > 0) {
+                    if (d.entry < 0) d.entry = i;
+                    d.last = i;
+                    d.chain[nchain++] = i;
+                }
+            }
+            for (int k = 0; k + 1 < nchain; ++k) d.next[d.chain[k]] = d.chain[k + 1];
+            if (d.entry < 0) fail(CG_ERR_NO_DEPLOYED_STAGE, "plan deploys no stage");
+        }
+        auto* res = new cg_sim_result{};
+        res->n = n;
+        *out = res;
+        if (P == 0) return;
+        SimRunBuffers& B = E->simbuf;
+        cudaStream_t s = E->s;
+        auto dev = [&](DevBuf& b, const double* src, size_t count) -> const double* {
+            if (tr->on_device) return src;
+            double* d = b.as<double>(std::max<size_t>(1, count));
+            CG_CUDA(cudaMemcpyAsync(d, src, count * 8, cudaMemcpyHostToDevice, s));
+            return d;
+        };
+        SimRunArgs a{};
+        a.n = n;
+        a.arrival = dev(B.arr, tr->arrival_s, (size_t)n);
+        a.in = dev(B.in, tr->input_tokens, (size_t)n);
+        a.out = dev(B.out, tr->output_tokens, (size_t)C * n);
+        a.scores = dev(B.sc, tr->scores, (size_t)C * n);
+        auto up = [&](DevBuf& b, const std::vector<double>& v) {
+            double* d = b.as<double>(std::max<size_t>(1, v.size()));
+            if (!v.empty()) CG_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s));
+            return d;
+        };
+        a.ppt = up(B.ppt, ppt);
+        a.pf = up(B.pf, pfix);
+        a.dpt = up(B.dpt, dpt);
+        std::vector<double> scales(cfg->slo_scales, cfg->slo_scales + cfg->num_scales);
+        a.scales = up(B.scales, scales);
+        a.nscales = cfg->num_scales;
+        const long long warmup = (long long)(size_t)(cfg->warmup_fraction * (double)n);
+        a.warmup = warmup;
+        const int base_mode = cfg->slo_base_s > 0 ? 0 : (compare ? 2 : 1);
+        int launches = 0;
+        std::vector<SimPlanOut> o;
+        sim_run_batch(B, s, a, desc, C, base_mode, cfg->slo_base_s, &launches, o);
+        double arr_w = 0.0;
+        if (warmup < n) {
+            if (tr->on_device) {
+                CG_CUDA(cudaMemcpyAsync(&arr_w, tr->arrival_s + warmup, 8, cudaMemcpyDeviceToHost, s));
+                CG_CUDA(cudaStreamSynchronize(s));
+            } else {
+                arr_w = tr->arrival_s[warmup];
+            }
+        }
+        res->reports = static_cast<cg_sim_report*>(std::calloc((size_t)P, sizeof(cg_sim_report)));
+        res->num_reports = P;
+        const long long m = n - warmup;
+        for (int pi = 0; pi < P; ++pi) {
+            cg_sim_report& r = res->reports[pi];
+            SimPlanOut& x = o[pi];
+            r.end_to_end_s = static_cast<double*>(std::malloc(sizeof(double) * n));
+            r.accept_stage = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * n));
+            std::memcpy(r.end_to_end_s, x.e2e.data(), sizeof(double) * n);
+            std::memcpy(r.accept_stage, x.stage.data(), sizeof(int32_t) * n);
+            r.slo_base_s = x.base;
+            if (m > 0) {  // simulator.cpp:259-274
+                r.p95_s = x.p95;
+                const double span = x.last_completion - arr_w;
+                r.throughput_rps = span > 0 ? static_cast<double>(m) / span : 0.0;
+            }
+            r.num_scales = cfg->num_scales;
+            r.attainment_scale = static_cast<double*>(std::malloc(sizeof(double) * std::max(1, cfg->num_scales)));
+            r.attainment_fraction = static_cast<double*>(std::malloc(sizeof(double) * std::max(1, cfg->num_scales)));
+            const double considered = static_cast<double>(n - warmup);
+            for (int k = 0; k < cfg->num_scales; ++k) {  // attainment_curve (simulator.cpp:301-316)
+                r.attainment_scale[k] = cfg->slo_scales[k];
+                r.attainment_fraction[k] = considered > 0 ? (double)x.ok[k] / considered : 1.0;
+                if (!r.has_min_scale_95 && r.attainment_fraction[k] >= 0.95) {
+                    r.has_min_scale_95 = 1;
+                    r.min_scale_95 = cfg->slo_scales[k];
+                }
+            }
+            for (int st = 0; st < C; ++st) {  // queue-growth warning (simulator.cpp:280-296)
+                const long long size = x.served[st];
+                if (desc[pi].dp[st] == 0 || size < 8) continue;
+                const long long half = size / 2;
+                const double w1 = x.w1[st] / static_cast<double>(half);
+                const double w2 = x.w2[st] / static_cast<double>(size - half);
+                const double mean_service = x.service_sum[st] / static_cast<double>(size);
+                if (w2 > 2.0 * w1 && w2 > mean_service && r.num_unstable < 8) r.unstable_stages[r.num_unstable++] = st + 1;
+            }
+        }
+        res->gpu_launches = launches;
+        res->ms_total = tm.ms();
+    });
+}
 
 void cg_trace_buffer_free(cg_trace_buffer* b) {
     if (!b) return;

@@ -9,6 +9,7 @@ Names, argument meaning and error behaviour follow the reference C++ API:
     solve_min_max(table, total_gpus)                   cascade::innerplan::solve_min_max
     generate_trace(spec, seed)                         cascade::cli::generate_trace
     read_trace_jsonl(path)                             cascade::read_trace_jsonl
+    simulate(plan, ...) / compare(plans, ...)          cascade::sim::run / sim::compare
 
 Results are returned in the reference's JSON schema (plain dicts, the
 structure nlohmann::json(SweepResult) produces), errors raise CascadeError
@@ -156,6 +157,70 @@ class TraceBufferC(ctypes.Structure):
     _fields_ = [("host", Trace), ("device", Trace), ("stats", IngestStats)]
 
 
+class SimConfigC(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("slo_base_s", ctypes.c_double), ("slo_scales", _DP),
+                ("num_scales", ctypes.c_int32), ("warmup_fraction", ctypes.c_double)]
+
+
+class CascadePlanC(ctypes.Structure):
+    _fields_ = [("allocations", ctypes.POINTER(ctypes.c_int32)), ("processing_ratios", _DP), ("thresholds", _DP),
+                ("has_plan", ctypes.POINTER(ctypes.c_int32)), ("gpus_used", ctypes.POINTER(ctypes.c_int32)),
+                ("dp", ctypes.POINTER(ctypes.c_int32)), ("replicas", ctypes.POINTER(Replica))]
+
+
+class SimReportC(ctypes.Structure):
+    _fields_ = [("end_to_end_s", _DP), ("accept_stage", ctypes.POINTER(ctypes.c_int32)), ("p95_s", ctypes.c_double),
+                ("throughput_rps", ctypes.c_double), ("num_scales", ctypes.c_int32), ("attainment_scale", _DP),
+                ("attainment_fraction", _DP), ("has_min_scale_95", ctypes.c_int32), ("min_scale_95", ctypes.c_double),
+                ("slo_base_s", ctypes.c_double), ("num_unstable", ctypes.c_int32),
+                ("unstable_stages", ctypes.c_int32 * 8)]
+
+
+class SimResultC(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("num_reports", ctypes.c_int32), ("reports", ctypes.POINTER(SimReportC)),
+                ("gpu_launches", ctypes.c_int32), ("ms_total", ctypes.c_double)]
+
+
+SIM_DEFAULT_SCALES = [1, 1.5, 2, 2.5, 3, 4, 5, 6, 8, 10, 12, 14, 16, 20]
+
+
+def sim_config_c(cfg: Optional[dict]):
+    cfg = cfg or {}
+    scales = [float(v) for v in cfg.get("slo_scales", SIM_DEFAULT_SCALES)]
+    arr = (ctypes.c_double * max(1, len(scales)))(*scales)
+    return SimConfigC(int(cfg.get("seed", 0)), float(cfg.get("slo_base_s", 0.0)), arr, len(scales),
+                      float(cfg.get("warmup_fraction", 0.1))), arr
+
+
+def cascade_plan_c(plan: dict):
+    """CascadePlan JSON (domain.cpp:317-342 schema) -> cg_cascade_plan."""
+    C = len(plan["allocations"])
+    I32 = ctypes.c_int32
+    alloc = (I32 * C)(*[int(v) for v in plan["allocations"]])
+    ratios = (ctypes.c_double * C)(*[float(v) for v in plan["processing_ratios"]])
+    h = plan["thresholds"]["thresholds"]
+    thr = (ctypes.c_double * max(1, len(h)))(*[float(v) for v in h])
+    has = (I32 * C)(*[0 if p is None else 1 for p in plan["plans"]])
+    used = (I32 * C)(*[0 if p is None else int(p["gpus_used"]) for p in plan["plans"]])
+    dps = (I32 * C)(*[0 if p is None else len(p["replicas"]) for p in plan["plans"]])
+    reps = [r for p in plan["plans"] if p is not None for r in p["replicas"]]
+    rarr = (Replica * max(1, len(reps)))(*[Replica(int(r["tp"]), int(r["pp"])) for r in reps])
+    keep = (alloc, ratios, thr, has, used, dps, rarr)
+    return CascadePlanC(alloc, ratios, thr, has, used, dps, rarr), keep
+
+
+def _sim_report_json(r: SimReportC, n: int) -> dict:
+    e2e = np.ctypeslib.as_array(r.end_to_end_s, shape=(n,)) if n else np.zeros(0)
+    st = np.ctypeslib.as_array(r.accept_stage, shape=(n,)) if n else np.zeros(0, dtype=np.int32)
+    return {"per_request": [{"end_to_end_s": float(e2e[i]), "accept_stage": int(st[i])} for i in range(n)],
+            "p95_s": float(r.p95_s), "throughput_rps": float(r.throughput_rps),
+            "attainment": [{"scale": float(r.attainment_scale[k]), "fraction": float(r.attainment_fraction[k])}
+                           for k in range(r.num_scales)],
+            "min_scale_95": float(r.min_scale_95) if r.has_min_scale_95 else None,
+            "slo_base_s": float(r.slo_base_s),
+            "unstable_stages": [int(r.unstable_stages[k]) for k in range(r.num_unstable)]}
+
+
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
                                 ctypes.c_void_p)
 
@@ -163,7 +228,8 @@ EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_eng
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
             "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
             "cg_merge_row_shards", "cg_shard_range", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
-            "cg_trace_buffer_free", "cg_sweep_result_json", "cg_text_free"]
+            "cg_trace_buffer_free", "cg_sweep_result_json", "cg_text_free", "cg_simulate",
+            "cg_sim_result_free"]
 
 _lib = None
 
@@ -230,6 +296,13 @@ def library():
         L.cg_sweep_result_json.restype = Status
         L.cg_text_free.argtypes = [ctypes.c_void_p]
         L.cg_text_free.restype = None
+        L.cg_simulate.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), ctypes.POINTER(Model), ctypes.c_int32,
+                                  ctypes.POINTER(Hardware), ctypes.POINTER(CostParams), ctypes.POINTER(SimConfigC),
+                                  ctypes.POINTER(CascadePlanC), ctypes.c_int32, ctypes.c_int32,
+                                  ctypes.POINTER(ctypes.POINTER(SimResultC))]
+        L.cg_simulate.restype = Status
+        L.cg_sim_result_free.argtypes = [ctypes.POINTER(SimResultC)]
+        L.cg_sim_result_free.restype = None
         L.cg_trace_buffer_free.argtypes = [ctypes.POINTER(TraceBufferC)]
         L.cg_trace_buffer_free.restype = None
         L.cg_engine_stream.argtypes = [ctypes.c_void_p]
@@ -498,6 +571,44 @@ class Engine:
                     "scores": col(b.host.scores, C * n).reshape(C, n)}
         finally:
             self._lib.cg_trace_buffer_free(out)
+
+    # -- cascade::sim::run / sim::compare (validation simulator)
+    def _simulate(self, trace, plans, models, hw, params, cfg, compare):
+        tb = _as_trace(trace)
+        tc = tb.c()
+        marr, keep = models_c(models)
+        hwc = hardware_c(hw)
+        pc = params_c(params)
+        sc, keep_s = sim_config_c(cfg)
+        conv = [cascade_plan_c(p) for p in plans]
+        parr = (CascadePlanC * max(1, len(conv)))(*[c for c, _ in conv])
+        out = ctypes.POINTER(SimResultC)()
+        _check(self._lib.cg_simulate(self._h, ctypes.byref(tc), marr, len(models), ctypes.byref(hwc),
+                                     ctypes.byref(pc), ctypes.byref(sc), parr, len(conv), 1 if compare else 0,
+                                     ctypes.byref(out)))
+        try:
+            r = out.contents
+            self.last_sim = {"gpu_launches": int(r.gpu_launches), "ms_total": float(r.ms_total)}
+            return [_sim_report_json(r.reports[i], int(r.n)) for i in range(r.num_reports)]
+        finally:
+            self._lib.cg_sim_result_free(out)
+
+    def simulate(self, plan: dict, trace, models, hw: dict, params: Optional[dict] = None,
+                 cfg: Optional[dict] = None) -> dict:
+        """sim::run -> json(SimReport)."""
+        return self._simulate(trace, [plan], models, hw, params, cfg, False)[0]
+
+    def simulate_many(self, plans, trace, models, hw: dict, params: Optional[dict] = None,
+                      cfg: Optional[dict] = None) -> list:
+        """sim::run of every plan (independent runs, one GPU batch)."""
+        return self._simulate(trace, plans, models, hw, params, cfg, False)
+
+    def compare(self, plans, trace, models, hw: dict, params: Optional[dict] = None,
+                cfg: Optional[dict] = None) -> dict:
+        """sim::compare -> json(CompareResult)."""
+        reps = self._simulate(trace, plans, models, hw, params, cfg, True)
+        return {"rows": [{"p95_s": r["p95_s"], "throughput_rps": r["throughput_rps"],
+                          "min_scale_95": r["min_scale_95"]} for r in reps], "reports": reps}
 
     # -- cascade::routing::route_trace
     def route_trace(self, trace, thresholds: Sequence[float], deployed: Sequence[bool],
