@@ -61,19 +61,28 @@ __global__ void k_sr_dry(SimRunArgs a, const SimPlanDesc* __restrict__ plan, dou
     lat[r] = latency;
 }
 
-// ... summed in trace order and divided by n
-__global__ void k_sr_mean(const double* __restrict__ lat, long long n, double* __restrict__ out) {
+// ... summed in trace order and divided by n: the block stages tiles in shared
+// memory, thread 0 adds them sequentially (one block per plan)
+__global__ void __launch_bounds__(1024) k_sr_mean(const double* __restrict__ lat, long long n,
+                                                  double* __restrict__ out) {
+    constexpr int TILE = 2048;
+    __shared__ double tile[2][TILE];
+    const double* x = lat + (long long)blockIdx.x * n;
     double sum = 0.0;
-    long long r = 0;
-    for (; r + 4 <= n; r += 4) {
-        const double x0 = lat[r], x1 = lat[r + 1], x2 = lat[r + 2], x3 = lat[r + 3];
-        sum = __dadd_rn(sum, x0);
-        sum = __dadd_rn(sum, x1);
-        sum = __dadd_rn(sum, x2);
-        sum = __dadd_rn(sum, x3);
+    int buf = 0;
+    for (long long i = threadIdx.x; i < TILE && i < n; i += blockDim.x) tile[0][i] = x[i];
+    __syncthreads();
+    for (long long b0 = 0; b0 < n; b0 += TILE) {
+        const long long nb = b0 + TILE;
+        for (long long i = threadIdx.x; i < TILE && nb + i < n; i += blockDim.x) tile[buf ^ 1][i] = x[nb + i];
+        if (threadIdx.x == 0) {
+            const int len = (int)(n - b0 < TILE ? n - b0 : TILE);
+            for (int i = 0; i < len; ++i) sum = __dadd_rn(sum, tile[buf][i]);
+        }
+        __syncthreads();
+        buf ^= 1;
     }
-    for (; r < n; ++r) sum = __dadd_rn(sum, lat[r]);
-    *out = __ddiv_rn(sum, (double)n);
+    if (threadIdx.x == 0) out[blockIdx.x] = __ddiv_rn(sum, (double)n);
 }
 
 // One stage pass of every plan of the batch (warp per plan).
@@ -111,8 +120,9 @@ __global__ void __launch_bounds__(32 * SR_WARPS) k_sr_stage(SimRunArgs a, int st
     long long nesc = 0;
     const double* out_s = a.out + (long long)s * n;
     const double* sc_s = a.scores + (long long)s * n;
+    __shared__ double s_t[SR_WARPS][32], s_in[SR_WARPS][32], s_o[SR_WARPS][32];
     for (long long b = 0; b < m; b += 32) {
-        // lanes gather the next 32 events
+        // lanes gather the next 32 events (time, request, trace fields) ...
         const long long e = b + lane;
         double bt = 0.0, bin = 0.0, bout = 0.0, bsc = 0.0, barr = 0.0;
         long long br = 0;
@@ -124,86 +134,89 @@ __global__ void __launch_bounds__(32 * SR_WARPS) k_sr_stage(SimRunArgs a, int st
             bsc = sc_s[br];
             barr = a.arrival[br];
         }
+        __syncwarp();
+        s_t[warp][lane] = bt;
+        s_in[warp][lane] = bin;
+        s_o[warp][lane] = bout;
+        __syncwarp();
+        // ... and the warp walks them in order; event i's finish time ends up
+        // in lane i, outputs are written in parallel after the walk
         const int cnt = (int)(m - b < 32 ? m - b : 32);
+        double my_fin = 0.0;
+#pragma unroll 2
         for (int i = 0; i < cnt; ++i) {
-            const double t = __shfl_sync(0xffffffffu, bt, i);
-            const double in = __shfl_sync(0xffffffffu, bin, i);
-            const double o = __shfl_sync(0xffffffffu, bout, i);
-            // join shortest expected work (simulator.cpp:215-224)
+            const double t = s_t[warp][i];
+            const double in = s_in[warp][i];
+            const double o = s_o[warp][i];
+            // join shortest expected work (simulator.cpp:215-224): the lowest
+            // idle replica (backlog max(0, avail - t) == 0), else the minimum
+            // (backlog, index) -- backlogs > 0, so their bit patterns order
+            // like the values: hi word, lo word, then index, by warp reductions
             int win = -1;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const bool idle = (r * 32 + lane) < dp && avail[r] <= t;  // max(0, avail - t) == 0
+                const bool idle = (r * 32 + lane) < dp && avail[r] <= t;
                 const unsigned bal = __ballot_sync(0xffffffffu, idle);
                 if (win < 0 && bal) win = r * 32 + (__ffs(bal) - 1);
             }
-            if (win < 0) {  // every replica busy: (backlog, index) minimum
+            if (win < 0) {
                 unsigned long long kw = ~0ull;
                 int kj = 0x7fffffff;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int j = r * 32 + lane;
-                    if (j < dp) {
-                        const unsigned long long w =
-                            (unsigned long long)__double_as_longlong(__dsub_rn(avail[r], t));
-                        if (w < kw) {
-                            kw = w;
-                            kj = j;
-                        }
+                    const unsigned long long w = (unsigned long long)__double_as_longlong(__dsub_rn(avail[r], t));
+                    if (j < dp && w < kw) {
+                        kw = w;
+                        kj = j;
                     }
                 }
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    const unsigned long long ow = __shfl_xor_sync(0xffffffffu, kw, off);
-                    const int oj = __shfl_xor_sync(0xffffffffu, kj, off);
-                    if (ow < kw || (ow == kw && oj < kj)) {
-                        kw = ow;
-                        kj = oj;
-                    }
-                }
-                win = kj;
+                const unsigned hi = (unsigned)(kw >> 32);
+                const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+                const unsigned lo = hi == mhi ? (unsigned)kw : 0xffffffffu;
+                const unsigned mlo = __reduce_min_sync(0xffffffffu, lo);
+                const unsigned jj = (hi == mhi && lo == mlo) ? (unsigned)kj : 0xffffffffu;
+                win = (int)__reduce_min_sync(0xffffffffu, jj);
             }
+            // every lane prices its own replicas (off the selection's critical
+            // path); the winner keeps its finish time, the rest is broadcast
             const int wl = win & 31, wr = win >> 5;
-            double wav = 0.0, wppt = 0.0, wpf = 0.0, wdpt = 0.0;
+            double wstart = 0.0, wservice = 0.0;
 #pragma unroll
-            for (int r = 0; r < R; ++r)
+            for (int r = 0; r < R; ++r) {
+                const double st_r = (t < avail[r]) ? avail[r] : t;  // std::max(ev.time, avail)
+                const double sv_r = __dadd_rn(__dadd_rn(__dmul_rn(ppt[r], in), pf[r]), __dmul_rn(o, dpt[r]));
                 if (r == wr) {
-                    wav = avail[r];
-                    wppt = ppt[r];
-                    wpf = pf[r];
-                    wdpt = dpt[r];
+                    wstart = st_r;
+                    wservice = sv_r;
+                    if (lane == wl) avail[r] = __dadd_rn(st_r, sv_r);
                 }
-            wav = __shfl_sync(0xffffffffu, wav, wl);
-            wppt = __shfl_sync(0xffffffffu, wppt, wl);
-            wpf = __shfl_sync(0xffffffffu, wpf, wl);
-            wdpt = __shfl_sync(0xffffffffu, wdpt, wl);
-            const double start = (t < wav) ? wav : t;  // std::max(ev.time, avail)
-            const double service = __dadd_rn(__dadd_rn(__dmul_rn(wppt, in), wpf), __dmul_rn(o, wdpt));
+            }
+            const double start = __shfl_sync(0xffffffffu, wstart, wl);
+            const double service = __shfl_sync(0xffffffffu, wservice, wl);
             const double fin = __dadd_rn(start, service);
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-                if (r == wr && lane == wl) avail[r] = fin;
-            const long long ei = b + i;
+            if (lane == i) my_fin = fin;
             const double wait = __dsub_rn(start, t);
-            if (ei < half) w1 = __dadd_rn(w1, wait);
+            if (b + i < half) w1 = __dadd_rn(w1, wait);
             else w2 = __dadd_rn(w2, wait);
             ssum = __dadd_rn(ssum, service);
-            const double scv = __shfl_sync(0xffffffffu, bsc, i);
-            const long long rr = __shfl_sync(0xffffffffu, br, i);
-            const double arr = __shfl_sync(0xffffffffu, barr, i);
-            if (last || scv >= thr) {
-                if (lane == 0) {
-                    e2e[rr] = __dsub_rn(fin, arr);
-                    ast[rr] = s + 1;
-                }
-            } else {
-                if (lane == 0) {
-                    nk[nesc] = dbl_to_key(fin);
-                    nv[nesc] = (unsigned long long)rr;
-                }
-                ++nesc;
-            }
         }
+        // outputs of the 32 events: accepted -> per-request result, else an
+        // escalation appended in processing order (ballot compaction)
+        const bool valid = lane < cnt;
+        const bool acc = valid && (last || bsc >= thr);
+        if (acc) {
+            e2e[br] = __dsub_rn(my_fin, barr);
+            ast[br] = s + 1;
+        }
+        const bool esc = valid && !acc;
+        const unsigned eb = __ballot_sync(0xffffffffu, esc);
+        if (esc) {
+            const long long pos = nesc + __popc(eb & ((1u << lane) - 1u));
+            nk[pos] = dbl_to_key(my_fin);
+            nv[pos] = (unsigned long long)br;
+        }
+        nesc += __popc(eb);
     }
     if (lane == 0) {
         a.nx_count[pi] = nesc;
@@ -311,14 +324,16 @@ void sim_run_batch(SimRunBuffers& B, cudaStream_t s, SimRunArgs a, std::vector<S
     std::vector<double> hbase(P, cfg_base);
     if (base_mode != 0) {
         const int nb = base_mode == 2 ? 1 : P;
-        double* lat = B.lat.as<double>((size_t)n);
+        double* lat = B.lat.as<double>((size_t)nb * n);
         std::vector<double> b(nb);
         for (int pi = 0; pi < nb; ++pi) {
-            k_sr_dry<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, dplans + pi, lat);
-            k_sr_mean<<<1, 1, 0, s>>>(lat, n, dbase + pi);
+            k_sr_dry<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, dplans + pi, lat + (long long)pi * n);
             CG_LAUNCH_CHECK();
-            *launches += 2;
+            ++*launches;
         }
+        k_sr_mean<<<nb, 1024, 0, s>>>(lat, n, dbase);
+        CG_LAUNCH_CHECK();
+        ++*launches;
         CG_CUDA(cudaMemcpyAsync(b.data(), dbase, 8 * nb, cudaMemcpyDeviceToHost, s));
         CG_CUDA(cudaStreamSynchronize(s));
         for (int pi = 0; pi < P; ++pi) hbase[pi] = base_mode == 2 ? b[0] : b[pi];
