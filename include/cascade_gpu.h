@@ -21,6 +21,8 @@
  *                            include/cascade/domain.hpp:162, src/domain.cpp:361-387
  *   cg_simulate           <- cascade::sim::run / sim::compare (validation simulator)
  *                            include/cascade/simulator.hpp:69-88, src/simulator.cpp:177-334
+ *   cg_drift_windows      <- the windowing / statistics of cli::cmd_drift
+ *                            src/cli.cpp:101-131 (stats_of_records, compute_baseline), 216-300
  *   cg_sweep_result_json  <- nlohmann::json(SweepResult).dump(indent) / json(front).dump(indent)
  *                            (sweep.json / front.json, src/cli.cpp:121,165-172,
  *                            src/outerplan.cpp:20-59, src/domain.cpp:270-356)
@@ -389,6 +391,53 @@ cg_status cg_simulate(cg_engine* engine, const cg_trace* trace, const cg_model* 
                       const cg_hardware* hw, const cg_cost_params* params, const cg_sim_config* cfg,
                       const cg_cascade_plan* plans, int32_t num_plans, int32_t compare, cg_sim_result** out);
 void cg_sim_result_free(cg_sim_result* result);
+
+/* Drift detection (cli.cpp:216-300): windows [t0 + k*I, t0 + k*I + I) over a
+ * non-decreasing stream, per-window statistics of the first window_requests
+ * records, relative deviations against the baseline (null when the baseline
+ * value is 0).  Windows with no records or span <= 0 are omitted, as in the
+ * reference.  Errc empty_trace "drift stream is empty" for n = 0. */
+typedef struct cg_drift_policy {    /* cli::DriftPolicy (cli.hpp:23-27) */
+    int32_t window_requests;
+    double window_interval_s;
+    double rel_tolerance;
+} cg_drift_policy;
+
+typedef struct cg_drift_stats {     /* cli::DriftBaseline (cli.hpp:50-56) */
+    double arrival_rate;
+    double mean_input_tokens;
+    double mean_output_tokens;
+    double stage1_accept_rate;
+    int32_t has_h1;
+    double h1;
+} cg_drift_stats;
+
+typedef struct cg_drift_window {    /* cli::DriftWindowReport (cli.hpp:118-127) */
+    double start_s;
+    double span_s;
+    int32_t requests;
+    int32_t sampled;
+    int64_t first_record;           /* trace index of the window's first record */
+    cg_drift_stats stats;
+    double deviation[4];            /* arrival_rate, mean_input_tokens, mean_output_tokens, stage1_accept_rate */
+    int32_t deviation_is_null[4];
+    int32_t drifted[4];
+    int32_t any_drift;
+} cg_drift_window;
+
+typedef struct cg_drift_result {
+    int64_t num_windows;
+    cg_drift_window* windows;
+    int32_t drift_detected;
+} cg_drift_result;
+
+cg_status cg_drift_windows(cg_engine* engine, const cg_trace* stream, const cg_drift_stats* baseline,
+                           const cg_drift_policy* policy, cg_drift_result** out);
+void cg_drift_result_free(cg_drift_result* result);
+/* compute_baseline (cli.cpp:125-131): whole-trace statistics, h1 = the plan's
+ * first threshold when it has one, arrival rate = overall_arrival_rate. */
+cg_status cg_trace_baseline(cg_engine* engine, const cg_trace* trace, int32_t has_h1, double h1,
+                            cg_drift_stats* out);
 
 const char* cg_version(void);
 

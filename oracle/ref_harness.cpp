@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <map>
 #include <string>
 #include <vector>
@@ -308,6 +310,43 @@ char* ref_simulate(const double* arrival, const double* in_tok, const double* ou
             out = sim::run(plans.at(0), trace, cfg.models, cfg.hardware, cfg.cost_model, sc);
         }
         return ok(std::move(out), seconds_since(t0));
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// cli::cmd_drift (cli.cpp:216-334, replan off) on a stream given as SoA
+/// columns: the files it reads are written into work_dir; returns the
+/// drift_report.json document.  Also compute_baseline of the same stream
+/// with h1 (has_h1) as "baseline_of_stream".
+char* ref_drift(const double* arrival, const double* in_tok, const double* out_tok, const double* scores,
+                std::int64_t n, int c, const char* config_json, const char* baseline_json, const char* work_dir,
+                int has_h1, double h1) {
+    try {
+        namespace fs = std::filesystem;
+        fs::create_directories(work_dir);
+        const std::string dir(work_dir);
+        { std::ofstream(dir + "/config.json") << config_json; }
+        { std::ofstream(dir + "/baseline.json") << baseline_json; }
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        write_trace_jsonl(dir + "/stream.jsonl", trace);
+        cli::DriftArgs args;
+        args.config_path = dir + "/config.json";
+        args.baseline_path = dir + "/baseline.json";
+        args.trace_path = dir + "/stream.jsonl";
+        args.out_dir = dir + "/out";
+        const auto t0 = std::chrono::steady_clock::now();
+        auto res = cli::cmd_drift(args);
+        const double el = seconds_since(t0);
+        std::ifstream rep(res.report_path);
+        json out;
+        out["report"] = json::parse(rep);
+        CascadePlan plan;
+        if (has_h1) plan.thresholds.thresholds = {h1};
+        out["baseline_of_stream"] = cli::compute_baseline(trace, plan);
+        return ok(std::move(out), el);
     } catch (const CascadeError& e) {
         return fail(e);
     } catch (const std::exception& e) {

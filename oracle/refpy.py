@@ -47,6 +47,8 @@ def lib():
             "ref_pareto": [_D, _D, ctypes.c_int64],
             "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
             "ref_dump_sweep": [ctypes.c_char_p],
+            "ref_drift": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
+                          ctypes.c_char_p, ctypes.c_int, ctypes.c_double],
             "ref_simulate": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
                              ctypes.c_char_p, ctypes.c_int],
             "ref_write_trace_jsonl": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p],
@@ -199,3 +201,11 @@ def simulate(trace: dict, config: dict, plans: list, sim_cfg: dict, compare: boo
     keep, n, c = _trace_args(trace)
     return _unwrap(_call(lib().ref_simulate, *map(_ptr, keep), n, c, json.dumps(config).encode(),
                          json.dumps(plans).encode(), json.dumps(sim_cfg).encode(), 1 if compare else 0))
+
+
+def drift(trace: dict, config: dict, baseline: dict, work_dir: str, h1=None) -> dict:
+    """cmd_drift's drift_report.json ("report") and compute_baseline ("baseline_of_stream")."""
+    keep, n, c = _trace_args(trace)
+    return _unwrap(_call(lib().ref_drift, *map(_ptr, keep), n, c, json.dumps(config).encode(),
+                         json.dumps(baseline).encode(), work_dir.encode(), 0 if h1 is None else 1,
+                         0.0 if h1 is None else float(h1)))

@@ -29,6 +29,7 @@
 #include "cascade_gpu.h"
 #include "cg_cuda.h"
 #include "cg_ingest.h"
+#include "cg_drift.h"
 #include "cg_json.h"
 #include "cg_simrun.h"
 #include "cg_internal.h"
@@ -162,6 +163,7 @@ struct cg_engine {
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
+    DriftBuffers driftbuf;
 };
 
 namespace {
@@ -875,6 +877,114 @@ cg_status cg_sweep_result_json(cg_engine* E, const cg_sweep_result* r, int32_t i
 }
 
 void cg_text_free(char* text) { std::free(text); }
+
+static DriftArgs drift_args(cg_engine* E, const cg_trace* tr) {
+    DriftBuffers& B = E->driftbuf;
+    const long long n = tr->n;
+    auto dev = [&](DevBuf& b, const double* src) -> const double* {
+        if (tr->on_device) return src;
+        double* d = b.as<double>((size_t)std::max<long long>(1, n));
+        CG_CUDA(cudaMemcpyAsync(d, src, (size_t)n * 8, cudaMemcpyHostToDevice, E->s));
+        return d;
+    };
+    DriftArgs a{};
+    a.n = n;
+    a.arrival = dev(B.arr, tr->arrival_s);
+    a.in = dev(B.in, tr->input_tokens);
+    a.out0 = dev(B.out0, tr->output_tokens);  // stage 1 = rows [0, n)
+    a.score0 = dev(B.sc0, tr->scores);
+    return a;
+}
+
+static double host_at(cg_engine* E, const cg_trace* tr, const double* col, long long i) {
+    if (!tr->on_device) return col[i];
+    double v = 0;
+    CG_CUDA(cudaMemcpyAsync(&v, col + i, 8, cudaMemcpyDeviceToHost, E->s));
+    CG_CUDA(cudaStreamSynchronize(E->s));
+    return v;
+}
+
+cg_status cg_drift_windows(cg_engine* E, const cg_trace* tr, const cg_drift_stats* base, const cg_drift_policy* pol,
+                           cg_drift_result** out) {
+    return guarded([&] {
+        if (!E || !tr || !base || !pol || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        *out = nullptr;
+        if (tr->n <= 0) fail(CG_ERR_EMPTY_TRACE, "drift stream is empty");
+        if (tr->stages < 1) fail(CG_ERR_INVALID_INPUT, "drift stream has no stages");
+        DriftArgs a = drift_args(E, tr);
+        a.t0 = host_at(E, tr, tr->arrival_s, 0);
+        a.stream_end = host_at(E, tr, tr->arrival_s, tr->n - 1);
+        a.interval = pol->window_interval_s;
+        a.window_requests = pol->window_requests;
+        a.has_h1 = base->has_h1;
+        a.h1 = base->h1;
+        int launches = 0;
+        std::vector<DriftWindowOut> w;
+        drift_windows(E->driftbuf, E->s, a, w, &launches);
+        auto* res = new cg_drift_result{};
+        std::vector<cg_drift_window> keep;
+        for (const auto& x : w) {
+            if (!x.valid) continue;  // window.empty() || span <= 0 (cli.cpp:238)
+            cg_drift_window o{};
+            o.start_s = x.start;
+            o.span_s = x.span;
+            o.requests = (int32_t)x.requests;
+            o.first_record = x.first;
+            o.sampled = (int32_t)x.sampled;
+            o.stats = cg_drift_stats{x.rate, x.mean_in, x.mean_out, x.accept, base->has_h1, base->h1};
+            const double b4[4] = {base->arrival_rate, base->mean_input_tokens, base->mean_output_tokens,
+                                  base->stage1_accept_rate};
+            const double c4[4] = {x.rate, x.mean_in, x.mean_out, x.accept};
+            for (int q = 0; q < 4; ++q) {  // check() (cli.cpp:252-266)
+                if (b4[q] != 0.0) {
+                    const double d = std::abs(c4[q] - b4[q]) / std::abs(b4[q]);
+                    o.deviation[q] = d;
+                    o.drifted[q] = d > pol->rel_tolerance ? 1 : 0;
+                } else {
+                    o.deviation_is_null[q] = 1;
+                    o.drifted[q] = c4[q] != 0.0 ? 1 : 0;
+                }
+                o.any_drift |= o.drifted[q];
+            }
+            res->drift_detected |= o.any_drift;
+            keep.push_back(o);
+        }
+        res->num_windows = (int64_t)keep.size();
+        res->windows = static_cast<cg_drift_window*>(std::malloc(sizeof(cg_drift_window) * std::max<size_t>(1, keep.size())));
+        for (size_t i = 0; i < keep.size(); ++i) res->windows[i] = keep[i];
+        *out = res;
+    });
+}
+
+void cg_drift_result_free(cg_drift_result* r) {
+    if (!r) return;
+    std::free(r->windows);
+    delete r;
+}
+
+cg_status cg_trace_baseline(cg_engine* E, const cg_trace* tr, int32_t has_h1, double h1, cg_drift_stats* out) {
+    return guarded([&] {
+        if (!E || !tr || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
+        *out = cg_drift_stats{0, 0, 0, 1, has_h1, h1};
+        // overall_arrival_rate (domain.cpp:396-401)
+        double rate = 0.0;
+        if (tr->n >= 2) {
+            const double span = host_at(E, tr, tr->arrival_s, tr->n - 1) - host_at(E, tr, tr->arrival_s, 0);
+            rate = span <= 0.0 ? 0.0 : static_cast<double>(tr->n) / span;
+        }
+        out->arrival_rate = rate;
+        if (tr->n <= 0 || tr->stages < 1) return;  // stats_of_records of an empty trace
+        DriftArgs a = drift_args(E, tr);
+        a.has_h1 = has_h1;
+        a.h1 = h1;
+        double r3[3];
+        int launches = 0;
+        trace_baseline(E->driftbuf, E->s, a, r3, &launches);
+        out->mean_input_tokens = r3[0];
+        out->mean_output_tokens = r3[1];
+        out->stage1_accept_rate = r3[2];
+    });
+}
 
 void cg_sim_result_free(cg_sim_result* r) {
     if (!r) return;

@@ -181,6 +181,38 @@ class SimResultC(ctypes.Structure):
                 ("gpu_launches", ctypes.c_int32), ("ms_total", ctypes.c_double)]
 
 
+class DriftPolicyC(ctypes.Structure):
+    _fields_ = [("window_requests", ctypes.c_int32), ("window_interval_s", ctypes.c_double),
+                ("rel_tolerance", ctypes.c_double)]
+
+
+class DriftStatsC(ctypes.Structure):
+    _fields_ = [("arrival_rate", ctypes.c_double), ("mean_input_tokens", ctypes.c_double),
+                ("mean_output_tokens", ctypes.c_double), ("stage1_accept_rate", ctypes.c_double),
+                ("has_h1", ctypes.c_int32), ("h1", ctypes.c_double)]
+
+
+class DriftWindowC(ctypes.Structure):
+    _fields_ = [("start_s", ctypes.c_double), ("span_s", ctypes.c_double), ("requests", ctypes.c_int32),
+                ("sampled", ctypes.c_int32), ("first_record", ctypes.c_int64), ("stats", DriftStatsC),
+                ("deviation", ctypes.c_double * 4), ("deviation_is_null", ctypes.c_int32 * 4),
+                ("drifted", ctypes.c_int32 * 4), ("any_drift", ctypes.c_int32)]
+
+
+class DriftResultC(ctypes.Structure):
+    _fields_ = [("num_windows", ctypes.c_int64), ("windows", ctypes.POINTER(DriftWindowC)),
+                ("drift_detected", ctypes.c_int32)]
+
+
+DRIFT_STATS = ["arrival_rate", "mean_input_tokens", "mean_output_tokens", "stage1_accept_rate"]
+
+
+def _drift_stats_json(s: DriftStatsC) -> dict:
+    return {"arrival_rate": s.arrival_rate, "mean_input_tokens": s.mean_input_tokens,
+            "mean_output_tokens": s.mean_output_tokens, "stage1_accept_rate": s.stage1_accept_rate,
+            "h1": s.h1 if s.has_h1 else None}
+
+
 SIM_DEFAULT_SCALES = [1, 1.5, 2, 2.5, 3, 4, 5, 6, 8, 10, 12, 14, 16, 20]
 
 
@@ -229,7 +261,7 @@ EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_eng
             "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
             "cg_merge_row_shards", "cg_shard_range", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
             "cg_trace_buffer_free", "cg_sweep_result_json", "cg_text_free", "cg_simulate",
-            "cg_sim_result_free"]
+            "cg_sim_result_free", "cg_drift_windows", "cg_drift_result_free", "cg_trace_baseline"]
 
 _lib = None
 
@@ -301,6 +333,14 @@ def library():
                                   ctypes.POINTER(CascadePlanC), ctypes.c_int32, ctypes.c_int32,
                                   ctypes.POINTER(ctypes.POINTER(SimResultC))]
         L.cg_simulate.restype = Status
+        L.cg_drift_windows.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), ctypes.POINTER(DriftStatsC),
+                                       ctypes.POINTER(DriftPolicyC), ctypes.POINTER(ctypes.POINTER(DriftResultC))]
+        L.cg_drift_windows.restype = Status
+        L.cg_drift_result_free.argtypes = [ctypes.POINTER(DriftResultC)]
+        L.cg_drift_result_free.restype = None
+        L.cg_trace_baseline.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), ctypes.c_int32, ctypes.c_double,
+                                        ctypes.POINTER(DriftStatsC)]
+        L.cg_trace_baseline.restype = Status
         L.cg_sim_result_free.argtypes = [ctypes.POINTER(SimResultC)]
         L.cg_sim_result_free.restype = None
         L.cg_trace_buffer_free.argtypes = [ctypes.POINTER(TraceBufferC)]
@@ -609,6 +649,44 @@ class Engine:
         reps = self._simulate(trace, plans, models, hw, params, cfg, True)
         return {"rows": [{"p95_s": r["p95_s"], "throughput_rps": r["throughput_rps"],
                           "min_scale_95": r["min_scale_95"]} for r in reps], "reports": reps}
+
+    # -- cli::cmd_drift windowing (drift detection) and compute_baseline
+    def drift_windows(self, stream, baseline: dict, policy: Optional[dict] = None) -> dict:
+        """{"windows": [...], "drift_detected": bool} in drift_report.json's schema."""
+        policy = dict({"window_requests": 100, "window_interval_s": 600.0, "rel_tolerance": 0.2}, **(policy or {}))
+        tb = _as_trace(stream)
+        tc = tb.c()
+        h1 = baseline.get("h1")
+        bc = DriftStatsC(float(baseline["arrival_rate"]), float(baseline["mean_input_tokens"]),
+                         float(baseline["mean_output_tokens"]), float(baseline["stage1_accept_rate"]),
+                         0 if h1 is None else 1, 0.0 if h1 is None else float(h1))
+        pc = DriftPolicyC(int(policy["window_requests"]), float(policy["window_interval_s"]),
+                          float(policy["rel_tolerance"]))
+        out = ctypes.POINTER(DriftResultC)()
+        _check(self._lib.cg_drift_windows(self._h, ctypes.byref(tc), ctypes.byref(bc), ctypes.byref(pc),
+                                          ctypes.byref(out)))
+        try:
+            r = out.contents
+            wins = []
+            for i in range(r.num_windows):
+                w = r.windows[i]
+                wins.append({"start_s": w.start_s, "span_s": w.span_s, "requests": int(w.requests),
+                             "sampled": int(w.sampled), "stats": _drift_stats_json(w.stats),
+                             "deviations": {DRIFT_STATS[q]: (None if w.deviation_is_null[q] else w.deviation[q])
+                                            for q in range(4)},
+                             "drifted_stats": [DRIFT_STATS[q] for q in range(4) if w.drifted[q]],
+                             "any_drift": bool(w.any_drift)})
+            return {"windows": wins, "drift_detected": bool(r.drift_detected)}
+        finally:
+            self._lib.cg_drift_result_free(out)
+
+    def compute_baseline(self, trace, h1: Optional[float] = None) -> dict:
+        tb = _as_trace(trace)
+        tc = tb.c()
+        out = DriftStatsC()
+        _check(self._lib.cg_trace_baseline(self._h, ctypes.byref(tc), 0 if h1 is None else 1,
+                                           0.0 if h1 is None else float(h1), ctypes.byref(out)))
+        return _drift_stats_json(out)
 
     # -- cascade::routing::route_trace
     def route_trace(self, trace, thresholds: Sequence[float], deployed: Sequence[bool],
