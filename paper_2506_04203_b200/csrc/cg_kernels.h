@@ -164,6 +164,7 @@ struct SimGeometry {
 };
 
 int class_for_dp(int dpmax);
+void set_k4_pack(int p);
 void class_shape(int cls, int* W, int* R);
 void class_dp_range(int cls, int* lo, int* hi);
 SimGeometry sim_geometry(int cls, int mode, int sm_count);

@@ -146,6 +146,7 @@ struct cg_engine {
     int prune = 1;
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
+    int k4_pack = 1;  // lane packing of the JSQ kernel classes (see class_shape)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
@@ -240,6 +241,7 @@ int row_class(const HostPlanSpace& sp, int N) {
 void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vector<HostPlanSpace>& hs,
                    const cg_hardware& hw, const cg_cost_params& q, int N) {
     cg_engine& E = x.E;
+    set_k4_pack(E.k4_pack);
     const int nrows = (int)rows.size();
     const long long cells = (long long)nrows * (N + 1);
     const int n_req = q.queueing_sim_requests;
@@ -1280,6 +1282,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         if (k == "prune") e->prune = value ? 1 : 0;
         else if (k == "k1_form") e->k1_form = (int)value;
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
+        else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);

@@ -767,11 +767,18 @@ SimGeometry sim_geometry(int cls, int mode, int sm_count) {
     return g;
 }
 
+// Lane packing of the replica-count classes (engine option k4_pack):
+//   0: one replica per lane, W = 4/8/16/32 lanes for dp <= 4/8/16/32
+//   1: two replicas per lane from dp > 4 on (more plans per warp)
+//   2: up to four replicas per lane
+static int g_pack = 0;
+void set_k4_pack(int p) { g_pack = p < 0 ? 0 : (p > 2 ? 2 : p); }
+
 void class_shape(int cls, int* W, int* R) {
-    static const int Ws[7] = {4, 8, 16, 32, 32, 32, 32};
-    static const int Rs[7] = {1, 1, 1, 1, 2, 4, 8};
-    *W = Ws[cls];
-    *R = Rs[cls];
+    static const int Ws[3][7] = {{4, 8, 16, 32, 32, 32, 32}, {4, 4, 8, 16, 32, 32, 32}, {4, 4, 4, 8, 32, 32, 32}};
+    static const int Rs[3][7] = {{1, 1, 1, 1, 2, 4, 8}, {1, 2, 2, 2, 2, 4, 8}, {1, 2, 4, 4, 2, 4, 8}};
+    *W = Ws[g_pack][cls];
+    *R = Rs[g_pack][cls];
 }
 
 void class_dp_range(int cls, int* lo, int* hi) {
@@ -803,9 +810,20 @@ void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t 
     } else {
         switch (cls) {
             case 0: launch_sim_t<4, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
-            case 1: launch_sim_t<8, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
-            case 2: launch_sim_t<16, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
-            case 3: launch_sim_t<32, 1, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
+            case 1:
+                if (g_pack == 0) launch_sim_t<8, 1, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                else launch_sim_t<4, 2, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                return;
+            case 2:
+                if (g_pack == 0) launch_sim_t<16, 1, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                else if (g_pack == 1) launch_sim_t<8, 2, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                else launch_sim_t<4, 4, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                return;
+            case 3:
+                if (g_pack == 0) launch_sim_t<32, 1, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                else if (g_pack == 1) launch_sim_t<16, 2, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                else launch_sim_t<8, 4, MODE_LIST>(a, sm_count, s, launches, grid_out);
+                return;
             case 4: launch_sim_t<32, 2, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
             case 5: launch_sim_t<32, 4, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
             case 6: launch_sim_t<32, 8, MODE_LIST>(a, sm_count, s, launches, grid_out); return;
