@@ -120,6 +120,8 @@ struct SimArgs {
     int check_stable;                          // 1: items are not pre-filtered (seeds)
     int seeds;                                 // 1: count completions as seeding work
     const unsigned long long* items;           // packed (row, plan) work items
+    const unsigned long long* parts;           // optional: the items' shape multisets (see encode_parts)
+    const unsigned long long* perm;            // optional: item i is items[perm[i]] (sorted lists)
     unsigned long long nitems;
     unsigned long long* item_counter;
     const RowDesc* rows;
@@ -152,6 +154,7 @@ struct FilterArgs {
     RowTables tab;
     const unsigned long long* ub;
     unsigned long long* lists[7];
+    unsigned long long* parts[7];              // shape multisets of the listed plans
     unsigned long long* keys[7];               // coarse service-bound order keys
     unsigned long long* list_count;            // [7]
     unsigned long long list_cap;               // per class

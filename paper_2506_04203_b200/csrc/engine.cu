@@ -81,6 +81,11 @@ struct Timer {
     }
 };
 
+__global__ void k_iota_u64(unsigned long long* p, long long n) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (unsigned long long)i;
+}
+
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -160,7 +165,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lidx;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -345,12 +350,15 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
 
     // Runs one packed work list through the class kernel, then the deep-queue
     // re-runs of its ring overflows.
-    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds) {
+    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
+                        const unsigned long long* parts, const unsigned long long* perm) {
         if (nitems == 0) return;
         CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
         CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
         SimArgs a = base;
         a.items = items;
+        a.parts = parts;
+        a.perm = perm;
         a.nitems = nitems;
         a.check_stable = seeds ? 1 : 0;
         a.seeds = seeds ? 1 : 0;
@@ -367,6 +375,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
             SimArgs d = a;
             d.items = ovf;
+            d.parts = nullptr;
+            d.perm = nullptr;
             d.nitems = novf;
             d.ring_global = ring;
             d.ovf_count = ovfcnt2;
@@ -394,7 +404,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         if (!seeds.empty()) {
             unsigned long long* dseeds = E.d_seeds.as<unsigned long long>(seeds.size());
             x.h2d(dseeds, seeds.data(), seeds.size() * 8);
-            run_list(dseeds, seeds.size(), 3, true);
+            run_list(dseeds, seeds.size(), 3, true, nullptr, nullptr);
         }
     }
     // Filter waves: enumerate every plan once, keep stable + not-bounded plans
@@ -409,6 +419,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         const unsigned long long wave_chunks = (16ull << 20) / chunk;
         const unsigned long long cap = wave_chunks * chunk;
         unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
+        unsigned long long* lparts = E.d_lparts.as<unsigned long long>((size_t)7 * cap);
+        unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cap);
         unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* tk = E.d_lk1.as<unsigned long long>(cap);
         unsigned long long* tv = E.d_lv1.as<unsigned long long>(cap);
@@ -434,6 +446,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fa.ub = ub;
             for (int c = 0; c < 7; ++c) {
                 fa.lists[c] = lists + (size_t)c * cap;
+                fa.parts[c] = lparts + (size_t)c * cap;
                 fa.keys[c] = lkeys + (size_t)c * cap;
             }
             fa.list_count = lcount;
@@ -445,12 +458,16 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             x.sync();
             for (int c = 6; c >= 0; --c) {
                 unsigned long long* items = lists + (size_t)c * cap;
-                if (E.prune && counts[c] > 1) {  // ascending service bound (16-bit key: 2 passes)
-                    const int par = radix_sort_u64(lkeys + (size_t)c * cap, items, tk, tv, (long long)counts[c],
+                const unsigned long long* perm = nullptr;
+                if (E.prune && counts[c] > 1) {  // ascending service bound (16-bit key: 2 passes) of slot indices
+                    k_iota_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(tidx, (long long)counts[c]);
+                    CG_LAUNCH_CHECK();
+                    ++x.launches;
+                    const int par = radix_sort_u64(lkeys + (size_t)c * cap, tidx, tk, tv, (long long)counts[c],
                                                    0xffffull, rsh, x.s, &x.launches);
-                    if (par) items = tv;
+                    perm = par ? tv : tidx;
                 }
-                run_list(items, counts[c], c, false);
+                run_list(items, counts[c], c, false, lparts + (size_t)c * cap, perm);
             }
         }
     }

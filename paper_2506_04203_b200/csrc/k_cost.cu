@@ -132,8 +132,27 @@ struct GroupShared {
     int status;
     int has_item;
     int dp_enum;  // replicas of the current count vector
+    int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
+    unsigned char pshape[4], pcount[4];
     unsigned char counts[kMaxShapes];
 };
+
+// A plan's shape multiset packed in 64 bits by the filter (which enumerates
+// the plan anyway), so acquiring it needs no unranking: bits 0-2 number of
+// parts (1..4; 0 = not packable), 3-11 GPUs used, then per part 5 bits shape
+// index + 8 bits count.
+__device__ __forceinline__ unsigned long long encode_parts(const unsigned char* c, int S, int used) {
+    unsigned long long v = 0;
+    int np = 0;
+    for (int s = 0; s < S; ++s) {
+        if (!c[s]) continue;
+        if (np == 4) return 0ull;
+        v |= ((unsigned long long)s | ((unsigned long long)c[s] << 5)) << (12 + 13 * np);
+        ++np;
+    }
+    if (used > 511) return 0ull;
+    return v | (unsigned long long)np | ((unsigned long long)used << 3);
+}
 
 // MODE: 0 = plan-index ranges (smem rings), 1 = explicit plan list (smem
 // rings; bound seeding), 2 = explicit list with global-memory rings (deep
@@ -184,14 +203,30 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
             gs.status = ST_DONE;
             return;
         }
-        const unsigned long long item = a.items[it];
+        const unsigned long long slot = a.perm ? (unsigned long long)a.perm[it] : it;
+        const unsigned long long item = a.items[slot];
+        const unsigned long long pk = a.parts ? a.parts[slot] : 0ull;
         const int row = (int)(item >> kItemPlanBits);
         const unsigned long long plan = item & kItemPlanMask;
         const RowDesc& rd = a.rows[row];
         const PlanSpace& sp = a.spaces[rd.space];
-        gs.used = unrank_plan(sp, plan, gs.counts);
         int dp = 0;
-        for (int s = 0; s < sp.S; ++s) dp += gs.counts[s];
+        const int np = (int)(pk & 7ull);
+        if (np > 0) {
+            for (int s = 0; s < sp.S; ++s) gs.counts[s] = 0;
+            for (int q = 0; q < np; ++q) {
+                const unsigned v = (unsigned)(pk >> (12 + 13 * q)) & 0x1fffu;
+                gs.pshape[q] = (unsigned char)(v & 31u);
+                gs.pcount[q] = (unsigned char)(v >> 5);
+                gs.counts[v & 31u] = (unsigned char)(v >> 5);
+                dp += (int)(v >> 5);
+            }
+            gs.used = (int)((pk >> 3) & 511ull);
+        } else {
+            gs.used = unrank_plan(sp, plan, gs.counts);
+            for (int s = 0; s < sp.S; ++s) dp += gs.counts[s];
+        }
+        gs.nparts = np;
         if (a.check_stable) {  // seeds are not pre-filtered
             const long long rb = (long long)row * kMaxShapes;
             bool good = true;
@@ -375,9 +410,17 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                         cnt[r] = head[r] = tail[r] = 0;
                         if (j < dp) {
                             int cum = 0, s = 0;
-                            for (; s < sp.S; ++s) {
-                                cum += gs.counts[s];
-                                if (j < cum) break;
+                            if (gs.nparts > 0) {
+                                for (int q = 0; q < gs.nparts; ++q) {
+                                    s = gs.pshape[q];
+                                    cum += gs.pcount[q];
+                                    if (j < cum) break;
+                                }
+                            } else {
+                                for (; s < sp.S; ++s) {
+                                    cum += gs.counts[s];
+                                    if (j < cum) break;
+                                }
                             }
                             pre[r] = a.tab.prefill[(long long)row * kMaxShapes + s];
                             dec[r] = a.tab.decode[(long long)row * kMaxShapes + s];
@@ -719,6 +762,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
                 if (slot < a.list_cap) {
                     a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | p;
+                    a.parts[cls][slot] = encode_parts(c, sp.S, used);
                     a.keys[cls][slot] = key;
                 }
             }
