@@ -186,6 +186,18 @@ def k1_at_scale(eng, torch, steps, warmup):
     return float(np.mean(ms)), bytes_per_launch, n, C, launches
 
 
+def committed_k4_issue():
+    """Time-weighted smsp__issue_active / warps_active of the K4 kernels from the
+    committed ncu --set full capture summary (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k4_ncu_summary.json")) as f:
+            d = json.load(f)
+        return {"issue_active_pct": d["issue_active_pct_time_weighted"],
+                "warps_active_pct": d["warps_active_pct_time_weighted"], "source": d["source"]}
+    except Exception:
+        return None
+
+
 def committed_k1_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per K1 launch from the
     committed ncu --set full capture summary (profiles/), or None."""
@@ -321,7 +333,8 @@ def run_ours(args):
             "roofline_k4": {"bound": "issue", "kernel": "k_sim (K4 JSQ simulation)", "ms_per_sweep": k4_ms,
                             "request_steps_per_s": steps_k4 / (k4_ms / 1000.0) if k4_ms > 0 else None,
                             "plans_simulated_full": st_dev[-1]["plans_simulated_full"],
-                            "plans_pruned": st_dev[-1]["plans_pruned"]},
+                            "plans_pruned": st_dev[-1]["plans_pruned"],
+                            "sm_issue_utilisation": committed_k4_issue()},
             "phases_ms": {k: float(np.mean([s[k] for s in st_dev])) for k in
                           ("ms_route", "ms_quality", "ms_rows", "ms_solve", "ms_total")},
             "clocks": clk.summary(),

@@ -18,10 +18,15 @@
 
 #include "cascade/cli.hpp"
 #include "cascade/outerplan.hpp"
+#include "cascade/simulator.hpp"
 #include "output_gpu.hpp"
 
 namespace cascade {
 std::vector<TraceRecord> cpu_read_trace_jsonl(const std::string& path);
+}
+namespace cascade::sim {
+SimReport cpu_run(const CascadePlan& plan, const std::vector<TraceRecord>& trace, const std::vector<ModelSpec>& models,
+                  const HardwareSpec& hw, const costmodel::CostModelParams& params, const SimConfig& cfg);
 }
 namespace cascade::outerplan {
 SweepResult cpu_sweep(const std::vector<TraceRecord>& trace, const std::vector<ModelSpec>& models,
@@ -96,6 +101,26 @@ int main(int argc, char** argv) {
     const bool writer_identical = gpu_sweep_text == cpu_sweep_text &&
                                   gpu_front_text == json(res.front).dump(2) + "\n";
 
+    // validation simulator: cmd_simulate's report.json (GPU sim::run) vs the
+    // reference body on the selected plan
+    bool sim_identical = true;
+    double gpu_sim_s = 0, cpu_sim_s = 0;
+    {
+        cli::SimulateArgs sargs;
+        sargs.config_path = cfg_path;
+        sargs.plan_path = out + "/gpu/plan.json";
+        sargs.trace_path = trace_path;
+        sargs.out_dir = out + "/gpu_sim";
+        t0 = std::chrono::steady_clock::now();
+        cli::cmd_simulate(sargs);
+        gpu_sim_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        sim::SimConfig sc;
+        t0 = std::chrono::steady_clock::now();
+        auto rep = sim::cpu_run(plan, tr, cfg.models, cfg.hardware, cfg.cost_model, sc);
+        cpu_sim_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        sim_identical = slurp(out + "/gpu_sim/report.json") == json(rep).dump(2) + "\n";
+    }
+
     if (!writer_identical) {  // keep both texts for inspection
         cli::write_output_file(out, "writer_gpu_sweep.json", gpu_sweep_text);
         cli::write_output_file(out, "writer_ref_sweep.json", cpu_sweep_text);
@@ -108,7 +133,10 @@ int main(int argc, char** argv) {
         report["files"][f] = {{"identical", a == b}, {"bytes", a.size()}};
         all = all && a == b;
     }
-    all = all && trace_identical && writer_identical;
+    all = all && trace_identical && writer_identical && sim_identical;
+    report["sim_identical"] = sim_identical;
+    report["gpu_sim_s"] = gpu_sim_s;
+    report["cpu_sim_s"] = cpu_sim_s;
     report["writer_identical"] = writer_identical;
     report["cpu_dump_s"] = cpu_dump_s;
     report["gpu_dump_s"] = gpu_dump_s;
