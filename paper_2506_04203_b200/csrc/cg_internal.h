@@ -54,6 +54,13 @@ struct RowTables {
     double* T;            // [row][ld] CRN arrivals (first n_req used)
     double* O;            // [row][ld] CRN outputs
     int ld;               // row stride: n_req rounded up to a multiple of 4 (32-byte rows)
+    // future-service bound: requests ranked by output (largest first) in
+    // blocks of 32; Pv[row][i] = the smallest output among the top 32(i+1),
+    // fut[c][i] = #{requests j >= 32c among the top 32(i+1)}
+    int nc;
+    const int* probe_req; // [nc] request index of block i's smallest output
+    double* Pv;           // [row][nc]
+    const unsigned* fut;  // [(nc+1)][nc]
 };
 
 struct SimItem {

@@ -151,6 +151,7 @@ struct cg_engine {
     int prune = 1;
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
+    int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
     int k4_pack = 1;  // lane packing of the JSQ kernel classes (see class_shape)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
@@ -165,7 +166,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lidx;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -259,6 +260,30 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     tab.decode = E.d_dec.as<double>((size_t)nrows * kMaxShapes);
     tab.mean_service = E.d_ms.as<double>((size_t)nrows * kMaxShapes);
     tab.ld = (n_req + 3) & ~3;
+    {
+        // future-service bound tables (RowTables): requests ranked by output,
+        // largest first (outputs are monotone in -L[2k+1], ties by index)
+        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
+        std::vector<int> desc(n_req), pos(n_req);
+        for (int k = 0; k < n_req; ++k) desc[k] = k;
+        std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
+        for (int k = 0; k < n_req; ++k) pos[desc[k]] = k;
+        const int nc = (n_req + 31) / 32;
+        std::vector<int> probe(nc);
+        for (int i = 0; i < nc; ++i) probe[i] = desc[std::min(32 * i + 31, n_req - 1)];
+        std::vector<unsigned> fut((size_t)(nc + 1) * nc, 0u);
+        for (int c = 0; c <= nc; ++c)
+            for (int j = 32 * c; j < n_req; ++j)
+                for (int i = pos[j] / 32; i < nc; ++i) ++fut[(size_t)c * nc + i];
+        int* dprobe = E.d_probe.as<int>((size_t)nc);
+        unsigned* dfut = E.d_fut.as<unsigned>(fut.size());
+        x.h2d(dprobe, probe.data(), probe.size() * sizeof(int));
+        x.h2d(dfut, fut.data(), fut.size() * sizeof(unsigned));
+        tab.nc = E.fut_bound ? nc : 0;
+        tab.probe_req = dprobe;
+        tab.fut = dfut;
+        tab.Pv = E.d_pv.as<double>((size_t)nrows * nc);
+    }
     tab.T = E.d_T.as<double>((size_t)nrows * tab.ld);
     tab.O = E.d_O.as<double>((size_t)nrows * tab.ld);
     CG_CUDA(cudaMemsetAsync(tab.T, 0, (size_t)nrows * tab.ld * 8, x.s));
@@ -1300,6 +1325,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k1_form") e->k1_form = (int)value;
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;
+        else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);

@@ -32,6 +32,9 @@
 //   * fp64 uses explicit _rn intrinsics, TU compiled with --fmad=false (H2).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "cg_cuda.h"
 #include "cg_internal.h"
 #include "cg_kernels.h"
@@ -116,6 +119,7 @@ __global__ void k_row_crn(RowSetupArgs a, const double* __restrict__ L) {
         const double x = __dmul_rn(neg_mean, L[2 * k + 1]);
         O[k] = (cap < x) ? cap : x;  // std::min(x, cap)
     }
+    for (int i = 0; i < a.tab.nc; ++i) a.tab.Pv[(long long)row * a.tab.nc + i] = O[a.tab.probe_req[i]];
 }
 
 // ---------------------------------------------------------------------------
@@ -189,6 +193,57 @@ __device__ __forceinline__ double service_bound(const SimArgs& a, int row, const
         lb = v < lb ? v : lb;
     }
     return lb * (1.0 - 1e-12) - 1e-12 * t_max;
+}
+
+// Future-service bound: the number of output-ranked blocks whose every
+// request has a service lower bound > U on every shape of the plan (the
+// qualifying blocks are a prefix, see RowTables).  Group-cooperative: lanes
+// take the blocks round-robin, the plan's shapes come from its parts (or
+// counts) in the group state.
+template <int W>
+__device__ __forceinline__ int future_blocks(const SimArgs& a, const GroupShared& gs, int row, bool active,
+                                             double U, int gl, int gshift, unsigned wmask, int lo0) {
+    const long long rb = (long long)row * kMaxShapes;
+    const double t_max = active ? a.tab.T[(long long)row * a.tab.ld + a.n_req - 1] : 0.0;
+    const int S = active ? a.spaces[a.rows[row].space].S : 0;
+    const bool bounded = active && U < __longlong_as_double(0x7ff0000000000000ll);
+    // W-ary search for the end of the qualifying prefix in [lo, hi)
+    int lo = active ? lo0 : 0, hi = active ? a.tab.nc : 0;
+    if (!bounded) hi = lo;
+    while (__any_sync(0xffffffffu, lo < hi)) {
+        const int len = hi - lo;
+        const int i = lo + (int)(((long long)(gl + 1) * len) / (W + 1));
+        bool qual = false;
+        if (lo < hi) {
+            const double o = a.tab.Pv[(long long)row * a.tab.nc + i];
+            double lb = __longlong_as_double(0x7ff0000000000000ll);
+            if (gs.nparts > 0) {
+                for (int p = 0; p < gs.nparts; ++p) {
+                    const int s = gs.pshape[p];
+                    const double v = a.tab.prefill[rb + s] + o * a.tab.decode[rb + s];
+                    lb = v < lb ? v : lb;
+                }
+            } else {
+                for (int s = 0; s < S; ++s) {
+                    if (!gs.counts[s]) continue;
+                    const double v = a.tab.prefill[rb + s] + o * a.tab.decode[rb + s];
+                    lb = v < lb ? v : lb;
+                }
+            }
+            qual = lb * (1.0 - 1e-12) - 1e-12 * t_max > U;
+        }
+        const unsigned b = (__ballot_sync(0xffffffffu, qual) >> gshift) & wmask;
+        const int t = __popc(b);  // qualifying probes form a prefix of the lanes
+        if (lo < hi) {
+            const int plo = lo + (int)(((long long)t * len) / (W + 1));        // probe t-1 position + 1 ...
+            const int phi = lo + (int)(((long long)(t + 1) * len) / (W + 1));  // ... probe t position
+            const int nlo = t > 0 ? plo + 1 : lo;
+            const int nhi = t < W ? phi : hi;
+            lo = nlo;
+            hi = nhi < nlo ? nlo : nhi;
+        }
+    }
+    return lo;
 }
 
 // Leader lane: pop the next (row, plan) work item of this kernel's list and
@@ -384,6 +439,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
         cnt[r] = head[r] = tail[r] = 0;
     }
     unsigned long long steps = 0, full = 0, pruned = 0;
+    int qi = 0;  // output-ranked blocks whose requests all exceed U on service alone
     const double INF = __longlong_as_double((long long)kInfBits);
 
     for (unsigned it = 0;; ++it) {
@@ -436,6 +492,17 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
             __syncwarp();
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
+        {
+            // the bound U is read by every lane from a concurrently tightened
+            // ub: make the group agree on one value (its leader's) so that
+            // every prune decision is group-uniform
+            U = __shfl_sync(FULL, U, gshift);
+            const bool fresh = need && status == ST_RUN;
+            if (a.prune && a.tab.nc > 0 && __any_sync(FULL, fresh)) {
+                const int q = future_blocks<W>(a, gs, row, fresh, U, gl, gshift, wmask, 0);
+                if (fresh) qi = q;
+            }
+        }
 
         // ---- phase B: UNROLL JSQ dispatch steps per running group.
         // k is a multiple of UNROLL here (plans start at k = 0 and advance
@@ -549,7 +616,10 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                 tot += __shfl_xor_sync(FULL, tot, off);
                 ov |= __shfl_xor_sync(FULL, ov, off);
             }
+            bool urefresh = false;
             if (status == ST_RUN) {
+                // requests still to come whose service alone exceeds U
+                const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
                 if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
@@ -557,14 +627,22 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
                     }
                     steps += k;
                     status = ST_NEED;
-                } else if (a.prune && tot >= a.K) {
+                } else if (a.prune && tot + fut >= a.K) {
                     pruned += 1;
                     steps += k;
                     status = ST_NEED;
                 } else if (a.prune) {
-                    U = __longlong_as_double(
+                    const double U2 = __longlong_as_double(
                         (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
+                    urefresh = U2 < U;
+                    U = U2;
                 }
+            }
+            U = __shfl_sync(FULL, U, gshift);
+            urefresh = __shfl_sync(FULL, urefresh ? 1 : 0, gshift) != 0;
+            if (a.tab.nc > 0 && __any_sync(FULL, urefresh)) {
+                const int q = future_blocks<W>(a, gs, row, urefresh, U, gl, gshift, wmask, qi);
+                if (urefresh) qi = q;
             }
             if (status == ST_NEED && gl == 0) gs.status = ST_NEED;
         }
@@ -844,6 +922,11 @@ int class_for_dp(int dpmax) {
 
 void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out) {
+    static const bool trace = std::getenv("CG_TRACE_K4") != nullptr;
+    if (trace && a.nitems > 0) {
+        std::fprintf(stderr, "[k4] cls=%d mode=%d items=%llu\n", cls, mode, (unsigned long long)a.nitems);
+        std::fflush(stderr);
+    }
     if (mode == MODE_DEEP) {
         switch (cls) {
             case 0: case 1: case 2: case 3: launch_sim_t<32, 1, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
