@@ -121,6 +121,7 @@ struct SimArgs {
     int seeds;                                 // 1: count completions as seeding work
     const unsigned long long* items;           // packed (row, plan) work items
     const unsigned long long* parts;           // optional: the items' shape multisets (see encode_parts)
+    const unsigned long long* parts2;          // optional: parts 4..7 and the part count (lane kernels)
     const unsigned long long* perm;            // optional: item i is items[perm[i]] (sorted lists)
     unsigned long long nitems;
     unsigned long long* item_counter;
@@ -135,7 +136,8 @@ struct SimArgs {
     unsigned long long* ovf;                   // packed items whose smem ring overflowed
     unsigned long long* ovf_count;
     unsigned long long ovf_cap;
-    double* scratch;                           // [slots][n_req]
+    double* scratch;                           // [slots][sld]
+    int sld;                                   // scratch column stride: n_req rounded up to 4
     double* ring_global;                       // DEEP: [warps][32*R*ring_cap]
     int ring_cap;
     unsigned long long* counters;
@@ -155,6 +157,7 @@ struct FilterArgs {
     const unsigned long long* ub;
     unsigned long long* lists[7];
     unsigned long long* parts[7];              // shape multisets of the listed plans
+    unsigned long long* parts2[7];             // their parts 4..7 (encode_parts)
     unsigned long long* keys[7];               // coarse service-bound order keys
     unsigned long long* list_count;            // [7]
     unsigned long long list_cap;               // per class

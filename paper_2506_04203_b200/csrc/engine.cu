@@ -152,7 +152,7 @@ struct cg_engine {
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
-    int k4_pack = 1;  // lane packing of the JSQ kernel classes (see class_shape)
+    int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
@@ -166,7 +166,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -247,7 +247,7 @@ int row_class(const HostPlanSpace& sp, int N) {
 void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vector<HostPlanSpace>& hs,
                    const cg_hardware& hw, const cg_cost_params& q, int N) {
     cg_engine& E = x.E;
-    set_k4_pack(E.k4_pack);
+    set_k4_pack(E.k4_pack == 3 && q.queueing_sim_requests > 65535 ? 1 : E.k4_pack);  // k_lane rings hold u16 request indices
     const int nrows = (int)rows.size();
     const long long cells = (long long)nrows * (N + 1);
     const int n_req = q.queueing_sim_requests;
@@ -347,7 +347,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         max_slots = std::max(max_slots, sim_geometry(cls, SIM_LIST, E.sm_count).slots);
         max_slots = std::max(max_slots, sim_geometry(cls, SIM_DEEP, E.sm_count).slots);
     }
-    double* scratch = E.d_scratch.as<double>((size_t)max_slots * n_req);
+    const int sld = (n_req + 3) & ~3;  // 32-byte scratch columns
+    double* scratch = E.d_scratch.as<double>((size_t)max_slots * sld);
     int ring_cap = 1;
     while (ring_cap < n_req) ring_cap <<= 1;
 
@@ -370,19 +371,22 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     base.ovf_count = ovfcnt;
     base.ovf_cap = (unsigned long long)E.ovf_cap;
     base.scratch = scratch;
+    base.sld = sld;
     base.counters = ctrs;
     base.ring_cap = ring_cap;
 
     // Runs one packed work list through the class kernel, then the deep-queue
     // re-runs of its ring overflows.
     auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
-                        const unsigned long long* parts, const unsigned long long* perm) {
+                        const unsigned long long* parts, const unsigned long long* parts2,
+                        const unsigned long long* perm) {
         if (nitems == 0) return;
         CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
         CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
         SimArgs a = base;
         a.items = items;
         a.parts = parts;
+        a.parts2 = parts2;
         a.perm = perm;
         a.nitems = nitems;
         a.check_stable = seeds ? 1 : 0;
@@ -401,6 +405,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             SimArgs d = a;
             d.items = ovf;
             d.parts = nullptr;
+            d.parts2 = nullptr;
             d.perm = nullptr;
             d.nitems = novf;
             d.ring_global = ring;
@@ -429,7 +434,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         if (!seeds.empty()) {
             unsigned long long* dseeds = E.d_seeds.as<unsigned long long>(seeds.size());
             x.h2d(dseeds, seeds.data(), seeds.size() * 8);
-            run_list(dseeds, seeds.size(), 3, true, nullptr, nullptr);
+            run_list(dseeds, seeds.size(), 3, true, nullptr, nullptr, nullptr);
         }
     }
     // Filter waves: enumerate every plan once, keep stable + not-bounded plans
@@ -445,6 +450,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         const unsigned long long cap = wave_chunks * chunk;
         unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* lparts = E.d_lparts.as<unsigned long long>((size_t)7 * cap);
+        unsigned long long* lparts2 = E.d_lparts2.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cap);
         unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* tk = E.d_lk1.as<unsigned long long>(cap);
@@ -472,6 +478,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             for (int c = 0; c < 7; ++c) {
                 fa.lists[c] = lists + (size_t)c * cap;
                 fa.parts[c] = lparts + (size_t)c * cap;
+                fa.parts2[c] = lparts2 + (size_t)c * cap;
                 fa.keys[c] = lkeys + (size_t)c * cap;
             }
             fa.list_count = lcount;
@@ -492,7 +499,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                                                    0xffffull, rsh, x.s, &x.launches);
                     perm = par ? tv : tidx;
                 }
-                run_list(items, counts[c], c, false, lparts + (size_t)c * cap, perm);
+                run_list(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm);
             }
         }
     }

@@ -137,25 +137,36 @@ struct GroupShared {
     int has_item;
     int dp_enum;  // replicas of the current count vector
     int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
-    unsigned char pshape[4], pcount[4];
+    unsigned char pshape[8], pcount[8];
     unsigned char counts[kMaxShapes];
 };
 
-// A plan's shape multiset packed in 64 bits by the filter (which enumerates
-// the plan anyway), so acquiring it needs no unranking: bits 0-2 number of
-// parts (1..4; 0 = not packable), 3-11 GPUs used, then per part 5 bits shape
-// index + 8 bits count.
-__device__ __forceinline__ unsigned long long encode_parts(const unsigned char* c, int S, int used) {
-    unsigned long long v = 0;
+// A plan's shape multiset packed by the filter (which enumerates the plan
+// anyway), so acquiring it needs no unranking.  Word 0: bits 0-2 number of
+// parts when it is <= 4 (0 otherwise), 3-11 GPUs used, then parts 0..3 (5 bits
+// shape index + 8 bits count each).  Word 1: bits 0-3 number of parts when it
+// is <= 8 (0 = not packable: unrank), then parts 4..7 in the same 13-bit form.
+struct PackedParts {
+    unsigned long long w0, w1;
+};
+__device__ __forceinline__ PackedParts encode_parts(const unsigned char* c, int S, int used) {
+    PackedParts v{0ull, 0ull};
     int np = 0;
     for (int s = 0; s < S; ++s) {
         if (!c[s]) continue;
-        if (np == 4) return 0ull;
-        v |= ((unsigned long long)s | ((unsigned long long)c[s] << 5)) << (12 + 13 * np);
+        if (np == 8) return PackedParts{0ull, 0ull};
+        const unsigned long long f = (unsigned long long)s | ((unsigned long long)c[s] << 5);
+        if (np < 4) v.w0 |= f << (12 + 13 * np);
+        else v.w1 |= f << (4 + 13 * (np - 4));
         ++np;
     }
-    if (used > 511) return 0ull;
-    return v | (unsigned long long)np | ((unsigned long long)used << 3);
+    if (used > 511) return PackedParts{0ull, 0ull};
+    v.w0 |= (unsigned long long)(np <= 4 ? np : 0) | ((unsigned long long)used << 3);
+    v.w1 |= (unsigned long long)np;
+    return v;
+}
+__device__ __forceinline__ unsigned part_field(const PackedParts& v, int q) {
+    return q < 4 ? (unsigned)(v.w0 >> (12 + 13 * q)) & 0x1fffu : (unsigned)(v.w1 >> (4 + 13 * (q - 4))) & 0x1fffu;
 }
 
 // MODE: 0 = plan-index ranges (smem rings), 1 = explicit plan list (smem
@@ -415,7 +426,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
 
     const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
     const long long slot = gwarp * G + gid;
-    double* scratch = a.scratch + slot * (long long)a.n_req;
+    double* scratch = a.scratch + slot * (long long)a.sld;
     double* gring = DEEP ? a.ring_global + gwarp * (long long)32 * R * a.ring_cap : nullptr;
     const int ring_mask = DEEP ? a.ring_cap - 1 : CAP - 1;
     const int ring_cap = DEEP ? a.ring_cap : CAP;
@@ -699,6 +710,502 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K4, lane-major form (replica-count classes 0-3).  A plan lives on W = 1, 2
+// or 4 lanes with R = 4 or 8 replicas per lane held in registers (replica
+// j = gl*R + r), so a warp carries 32/W plans and a request-step is a handful
+// of lane instructions instead of a group-wide exchange:
+//   * idle fast path: the lowest idle replica (avail <= t) wins, start = t;
+//     its FIFO is reset lazily (bit r of `lazy`: the replica holds exactly the
+//     job in service, finishing at avail[r]);
+//   * busy path (every replica of the plan busy): lazy FIFOs materialised,
+//     pops up to t, then the (in-system count, index) minimum -- the
+//     reference's argmin (costmodel.cpp:262-276);
+//   * prefill/decode of the lane's replicas in shared memory [r][lane]; the
+//     waiting jobs in shared-memory rings [r][slot][lane] of 16-bit request
+//     indices: a waiting job starts when its predecessor finishes, so its
+//     finish time is recomputed at pop time from the predecessor's,
+//     (nd + prefill) + out[k] * decode -- the same operands and operations as
+//     at dispatch, hence the same double.  Head/tail are packed 16+16 bits per
+//     replica (differences taken mod 2^16);
+//   * plans are claimed with one warp-aggregated atomic per round; the K-th
+//     largest selection is warp-cooperative, one finished plan at a time.
+// Exactness is that of k_sim: same operations in the same order per request.
+template <int W, int R>
+struct LaneTraits {
+    static constexpr int G = 32 / W;
+    static constexpr int CAP = R <= 4 ? 32 : 16;
+    static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
+    static constexpr size_t pd_bytes = (size_t)2 * R * 32 * sizeof(double);
+    static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
+    static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + hist_bytes + G * sizeof(GroupShared);
+};
+
+// Claims work item `it` into gs; false when the item is rejected (an unstable
+// seed, or a service bound above the live bound).
+__device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long it) {
+    const unsigned long long slot = a.perm ? (unsigned long long)a.perm[it] : it;
+    const unsigned long long item = a.items[slot];
+    PackedParts pk{0ull, 0ull};
+    if (a.parts && a.parts2) {
+        pk.w0 = a.parts[slot];
+        pk.w1 = a.parts2[slot];
+    }
+    const int row = (int)(item >> kItemPlanBits);
+    const unsigned long long plan = item & kItemPlanMask;
+    const RowDesc& rd = a.rows[row];
+    const PlanSpace& sp = a.spaces[rd.space];
+    const long long rb = (long long)row * kMaxShapes;
+    int np = (int)(pk.w1 & 15ull);
+    int dp = 0, used = 0;
+    if (np > 0) {
+        for (int q = 0; q < np; ++q) {
+            const unsigned v = part_field(pk, q);
+            gs.pshape[q] = (unsigned char)(v & 31u);
+            gs.pcount[q] = (unsigned char)(v >> 5);
+            dp += (int)(v >> 5);
+        }
+        used = (int)((pk.w0 >> 3) & 511ull);
+    } else {
+        used = unrank_plan(sp, plan, gs.counts);
+        for (int s = 0; s < sp.S; ++s) {
+            const int c = gs.counts[s];
+            if (!c) continue;
+            if (np < 8) {
+                gs.pshape[np] = (unsigned char)s;
+                gs.pcount[np] = (unsigned char)c;
+            }
+            ++np;
+            dp += c;
+        }
+        if (np > 8) np = 0;  // counts[] stay authoritative
+    }
+    if (a.check_stable) {  // seeds are not pre-filtered (costmodel.cpp:366-376)
+        double capacity = 0.0;
+        for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
+            const int sh = np > 0 ? gs.pshape[q] : s;
+            const int c = np > 0 ? gs.pcount[q] : gs.counts[s];
+            if (!c) continue;
+            if (!a.tab.shape_ok[rb + sh]) return false;
+            capacity = __dadd_rn(capacity, __ddiv_rn((double)c, a.tab.mean_service[rb + sh]));
+        }
+        if (rd.rate >= capacity) return false;
+    } else if (a.prune) {
+        const double U = __longlong_as_double(
+            (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
+        const double o_k = a.tab.O[(long long)row * a.tab.ld + a.kstar];
+        const double t_max = a.tab.T[(long long)row * a.tab.ld + a.n_req - 1];
+        double lb = __longlong_as_double(0x7ff0000000000000ll);
+        for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
+            const int sh = np > 0 ? gs.pshape[q] : s;
+            if (np == 0 && !gs.counts[s]) continue;
+            const double v = a.tab.prefill[rb + sh] + o_k * a.tab.decode[rb + sh];
+            lb = v < lb ? v : lb;
+        }
+        if (lb * (1.0 - 1e-12) - 1e-12 * t_max > U) {
+            atomicAdd(&a.counters[CTR_BOUND], 1ull);
+            return false;
+        }
+    }
+    gs.nparts = np;
+    gs.row = row;
+    gs.plan = plan;
+    gs.dp = dp;
+    gs.used = used;
+    return true;
+}
+
+template <int W, int R>
+__global__ void __launch_bounds__(128) k_lane(SimArgs a) {
+    using TR = LaneTraits<W, R>;
+    constexpr int G = TR::G;
+    constexpr int CAP = TR::CAP;
+    constexpr int UNROLL = 4;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gid = lane / W;
+    const int gl = lane % W;
+    const int gshift = gid * W;
+    const unsigned wmask = (W == 32) ? FULL : ((1u << W) - 1u);
+
+    unsigned char* wbase = smem + (size_t)warp * TR::bytes_per_warp;
+    unsigned short* ring = reinterpret_cast<unsigned short*>(wbase);
+    double* pre_s = reinterpret_cast<double*>(wbase + TR::ring_bytes);
+    double* dec_s = pre_s + R * 32;
+    unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
+    GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::hist_bytes);
+    GroupShared& gs = gsa[gid];
+
+    const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+    double* const scratch = a.scratch + (gwarp * G + gid) * (long long)a.sld;
+    const int n_req = a.n_req;
+    const double INF = __longlong_as_double((long long)kInfBits);
+
+    if (gl == 0) gs.status = ST_NEED;
+    __syncwarp();
+
+    int status = ST_NEED;
+    int row = 0, dp = 0, gpus = 0, k = 0, ab = 0, qi = 0;
+    unsigned long long plan = 0;
+    bool ovf = false;
+    unsigned lazy = 0;
+    double U = INF;
+    const double* Trow = a.tab.T;  // valid dummies until a plan is acquired
+    const double* Orow = a.tab.O;
+    // arrivals / outputs of the pair holding step k and of the next pair (prefetched)
+    double2 tq = make_double2(0.0, 0.0), oq = tq, tq2 = tq, oq2 = tq;
+    double avail[R], nd[R];
+    unsigned ht[R];  // head | tail << 16 of the waiting-job ring
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        avail[r] = INF;
+        nd[r] = INF;
+        ht[r] = 0;
+    }
+    unsigned long long steps = 0, full = 0, pruned = 0;
+
+    for (unsigned it = 0;; ++it) {
+        // ---- phase A: groups without a plan claim one (one atomic per round)
+        const bool need = status == ST_NEED;
+        if (__any_sync(FULL, need)) {
+            bool want = need && gl == 0;
+            unsigned m = __ballot_sync(FULL, want);
+            while (m) {
+                const int ldr = __ffs(m) - 1;
+                unsigned long long base = 0;
+                if (lane == ldr) base = atomicAdd(a.item_counter, (unsigned long long)__popc(m));
+                base = __shfl_sync(FULL, base, ldr);
+                bool again = false;
+                if (want) {
+                    const unsigned long long item = base + __popc(m & ((1u << lane) - 1u));
+                    if (item >= a.nitems) gs.status = ST_DONE;
+                    else if (lane_take(a, gs, item)) gs.status = ST_RUN;
+                    else again = true;
+                }
+                want = again;
+                m = __ballot_sync(FULL, want);
+            }
+            __syncwarp();
+            if (need) {
+                status = gs.status;
+                if (status == ST_RUN) {
+                    row = gs.row;
+                    dp = gs.dp;
+                    gpus = gs.used;
+                    plan = gs.plan;
+                    const long long rb = (long long)row * kMaxShapes;
+                    const int S = a.spaces[a.rows[row].space].S;
+                    Trow = a.tab.T + (long long)row * a.tab.ld;
+                    Orow = a.tab.O + (long long)row * a.tab.ld;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int j = gl * R + r;
+                        nd[r] = INF;
+                        ht[r] = 0;
+                        avail[r] = INF;
+                        if (j < dp) {
+                            int cum = 0, s = 0;
+                            if (gs.nparts > 0) {
+                                for (int q = 0; q < gs.nparts; ++q) {
+                                    s = gs.pshape[q];
+                                    cum += gs.pcount[q];
+                                    if (j < cum) break;
+                                }
+                            } else {
+                                for (; s < S; ++s) {
+                                    cum += gs.counts[s];
+                                    if (j < cum) break;
+                                }
+                            }
+                            pre_s[r * 32 + lane] = a.tab.prefill[rb + s];
+                            dec_s[r * 32 + lane] = a.tab.decode[rb + s];
+                            avail[r] = 0.0;
+                        }
+                    }
+                    k = 0;
+                    ab = 0;
+                    ovf = false;
+                    lazy = 0;
+                    tq = *reinterpret_cast<const double2*>(Trow);
+                    oq = *reinterpret_cast<const double2*>(Orow);
+                    tq2 = *reinterpret_cast<const double2*>(Trow + (n_req > 2 ? 2 : 0));
+                    oq2 = *reinterpret_cast<const double2*>(Orow + (n_req > 2 ? 2 : 0));
+                    U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus])
+                                : INF;
+                }
+            }
+            __syncwarp();
+        }
+        if (__all_sync(FULL, status == ST_DONE)) break;
+        {
+            U = __shfl_sync(FULL, U, gshift);  // one bound per group (leader's)
+            const bool fresh = need && status == ST_RUN;
+            if (a.prune && a.tab.nc > 0 && __any_sync(FULL, fresh)) {
+                const int q = future_blocks<W>(a, gs, row, fresh, U, gl, gshift, wmask, 0);
+                if (fresh) qi = q;
+            }
+        }
+
+        // ---- phase B: UNROLL request-steps per running plan, as pairs (rows
+        // and k are even-aligned) with the next pair's arrivals/outputs
+        // prefetched -- the lanes' rows differ, so they come from L2
+        auto step = [&](const double t, const double o) {
+            const bool run = status == ST_RUN;
+            unsigned m = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) m |= (avail[r] <= t) ? (1u << r) : 0u;
+            m = run ? m : 0u;
+            bool idle;
+            int wlane;
+            if (W == 1) {
+                idle = m != 0u;
+                wlane = gl;
+            } else {
+                const unsigned gb = (__ballot_sync(FULL, m != 0u) >> gshift) & wmask;
+                idle = gb != 0u;
+                wlane = __ffs(gb) - 1;
+            }
+            const bool busy = run && !idle;
+            int rr = __ffs(m) - 1;
+            double A = t;  // start time: t when a replica is idle, else avail of the chosen one
+            unsigned H = 0;
+            if (__any_sync(FULL, busy)) {
+                if (busy && lazy) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if ((lazy >> r) & 1u) {
+                            nd[r] = avail[r];
+                            ht[r] = (ht[r] & 0xffff0000u) | (ht[r] >> 16);
+                        }
+                    lazy = 0;
+                }
+                bool dep[R];
+                bool anydep = false;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    dep[r] = busy && nd[r] <= t;
+                    anydep |= dep[r];
+                }
+                while (__any_sync(FULL, anydep)) {
+                    anydep = false;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        if (dep[r]) {
+                            const unsigned h = ht[r] & 0xffffu;
+                            if (h != (ht[r] >> 16)) {  // next waiting job enters service
+                                const int kx = ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane];
+                                nd[r] = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
+                                                  __dmul_rn(Orow[kx], dec_s[r * 32 + lane]));
+                                ht[r] = (ht[r] & 0xffff0000u) | ((h + 1u) & 0xffffu);
+                            } else {
+                                nd[r] = INF;
+                            }
+                            dep[r] = nd[r] <= t;
+                            anydep |= dep[r];
+                        }
+                    }
+                }
+                // (in-system count << 9 | replica) minimum, as a tree
+                unsigned kk[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int j = gl * R + r;
+                    const unsigned c = (((ht[r] >> 16) - ht[r]) & 0xffffu) + (nd[r] < INF ? 1u : 0u);
+                    kk[r] = (j < dp) ? ((c << 9) | (unsigned)j) : 0xffffffffu;
+                }
+#pragma unroll
+                for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+                    for (int r = 0; r + w < R; r += 2 * w) kk[r] = kk[r + w] < kk[r] ? kk[r + w] : kk[r];
+                unsigned key = busy ? kk[0] : 0xffffffffu;
+#pragma unroll
+                for (int off = W / 2; off > 0; off >>= 1) {
+                    const unsigned v = __shfl_xor_sync(FULL, key, off);
+                    key = v < key ? v : key;
+                }
+                if (busy) {
+                    const int win = (int)(key & 511u);
+                    wlane = win / R;
+                    rr = win % R;
+                    // avail / ring state of replica rr: select tree on rr's bits
+                    double av[R];
+                    unsigned hv[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        av[r] = avail[r];
+                        hv[r] = ht[r];
+                    }
+#pragma unroll
+                    for (int w = 1; w < R; w <<= 1) {
+                        const bool hi = (rr & w) != 0;
+#pragma unroll
+                        for (int r = 0; r + w < R; r += 2 * w) {
+                            av[r] = hi ? av[r + w] : av[r];
+                            hv[r] = hi ? hv[r + w] : hv[r];
+                        }
+                    }
+                    A = av[0];  // > t: std::max(t, avail)
+                    H = hv[0];
+                }
+            }
+            const bool me = run && gl == wlane;
+            const int pidx = (me ? rr : 0) * 32 + lane;
+            const double fin = __dadd_rn(__dadd_rn(A, pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
+            const double soj = __dsub_rn(fin, t);
+            if (me) {
+                // idle: the FIFO now holds just this job (lazy reset; H = 0 is
+                // an empty ring).  Busy: the job joins the queue.
+                if (!idle) {
+                    ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
+                    H += 1u << 16;
+                    ovf |= (((H >> 16) - H) & 0xffffu) > (unsigned)CAP;
+                }
+                lazy |= idle ? (1u << rr) : 0u;
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r == rr) {
+                        avail[r] = fin;
+                        ht[r] = H;
+                    }
+                ab += soj > U ? 1 : 0;
+                scratch[k] = soj;
+            }
+            k += run ? 1 : 0;
+            status = (run && k == n_req) ? ST_FINISH : status;
+        };
+#pragma unroll 1
+        for (int u = 0; u < UNROLL; ++u) {
+            // k == u (mod 4) on every running lane, so the parity is warp-uniform
+            const bool odd = (u & 1) != 0;
+            const double t = odd ? tq.y : tq.x;
+            const double o = odd ? oq.y : oq.x;
+            if (odd) {
+                tq = tq2;
+                oq = oq2;
+                const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
+                tq2 = *reinterpret_cast<const double2*>(Trow + kp);
+                oq2 = *reinterpret_cast<const double2*>(Orow + kp);
+            }
+            step(t, o);
+        }
+
+        // ---- phase C: periodic exact-bound pruning and overflow checks
+        if ((it & (32u / UNROLL - 1u)) == (32u / UNROLL - 1u)) {
+            int tot = ab;
+            int ov = ovf ? 1 : 0;
+#pragma unroll
+            for (int off = W / 2; off > 0; off >>= 1) {
+                tot += __shfl_xor_sync(FULL, tot, off);
+                ov |= __shfl_xor_sync(FULL, ov, off);
+            }
+            bool urefresh = false;
+            if (status == ST_RUN) {
+                const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
+                if (ov) {
+                    if (gl == 0) {
+                        const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
+                        if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
+                    }
+                    steps += k;
+                    status = ST_NEED;
+                } else if (a.prune && tot + fut >= a.K) {
+                    pruned += 1;
+                    steps += k;
+                    status = ST_NEED;
+                } else if (a.prune) {
+                    const double U2 = __longlong_as_double(
+                        (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
+                    urefresh = U2 < U;
+                    U = U2;
+                }
+            }
+            U = __shfl_sync(FULL, U, gshift);
+            urefresh = __shfl_sync(FULL, urefresh ? 1 : 0, gshift) != 0;
+            if (a.tab.nc > 0 && __any_sync(FULL, urefresh)) {
+                const int q = future_blocks<W>(a, gs, row, urefresh, U, gl, gshift, wmask, qi);
+                if (urefresh) qi = q;
+            }
+            if (status == ST_NEED && gl == 0) gs.status = ST_NEED;
+        }
+
+        // ---- phase D: completed plans -> exact p95 (warp-cooperative) and row bookkeeping
+        if (__any_sync(FULL, status == ST_FINISH)) {
+            int tot = ab;
+            int ov = ovf ? 1 : 0;
+#pragma unroll
+            for (int off = W / 2; off > 0; off >>= 1) {
+                tot += __shfl_xor_sync(FULL, tot, off);
+                ov |= __shfl_xor_sync(FULL, ov, off);
+            }
+            bool sel = false;
+            if (status == ST_FINISH) {
+                steps += k;
+                if (ov) {
+                    if (gl == 0) {
+                        const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
+                        if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
+                    }
+                } else if (a.prune && tot >= a.K) {
+                    pruned += 1;
+                } else {
+                    sel = true;
+                }
+            }
+            __syncwarp();  // the columns' stores are visible to the whole warp
+            unsigned fm = __ballot_sync(FULL, sel && gl == 0);
+            while (fm) {
+                const int ldr = __ffs(fm) - 1;
+                fm &= fm - 1u;
+                const double* col = a.scratch + (gwarp * G + ldr / W) * (long long)a.sld;
+                const unsigned long long xb = group_kth_largest<32, true>(col, n_req, a.K, lane, FULL, 0, hist);
+                if (lane == ldr) {
+                    full += 1;
+                    const long long base = (long long)row * (a.N + 1);
+                    const unsigned long long old = atomicMin(&a.lat_min[base + gpus], xb);
+                    if (xb <= old) {
+                        const unsigned long long idx = atomicAdd(a.tie_count, 1ull);
+                        if (idx < a.tie_cap) a.ties[idx] = TieEntry{row, gpus, xb, plan};
+                    }
+                    for (int g2 = gpus; g2 <= a.N; ++g2) {
+                        unsigned long long* ub = &a.ub[base + g2];
+                        if (*(volatile unsigned long long*)ub <= xb) break;
+                        atomicMin(ub, xb);
+                    }
+                }
+                __syncwarp();
+            }
+            if (status == ST_FINISH) {
+                status = ST_NEED;
+                if (gl == 0) gs.status = ST_NEED;
+            }
+            __syncwarp();
+        }
+    }
+    if (gl == 0) {
+        count_add(&a.counters[CTR_STEPS], steps);
+        count_add(&a.counters[a.seeds ? CTR_SEED : CTR_FULL], full);
+        count_add(&a.counters[a.seeds ? CTR_SEED : CTR_PRUNED], pruned);
+    }
+}
+
+template <int W, int R>
+void launch_lane_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches, int* grid_out) {
+    using TR = LaneTraits<W, R>;
+    const size_t smem = TR::bytes_per_warp * 4;
+    auto kern = k_lane<W, R>;
+    CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int grid = sm_count * per_sm;
+    if (grid_out) *grid_out = grid;
+    if (a.nitems == 0) return;
+    kern<<<grid, 128, smem, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
+}
+
+// ---------------------------------------------------------------------------
 // K5: tie resolution and the prefix minimum over budgets
 
 __global__ void k_resolve_ties(ResolveArgs a) {
@@ -840,7 +1347,9 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
                 if (slot < a.list_cap) {
                     a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | p;
-                    a.parts[cls][slot] = encode_parts(c, sp.S, used);
+                    const PackedParts pk = encode_parts(c, sp.S, used);
+                    a.parts[cls][slot] = pk.w0;
+                    a.parts2[cls][slot] = pk.w1;
                     a.keys[cls][slot] = key;
                 }
             }
@@ -893,12 +1402,16 @@ SimGeometry sim_geometry(int cls, int mode, int sm_count) {
 //   0: one replica per lane, W = 4/8/16/32 lanes for dp <= 4/8/16/32
 //   1: two replicas per lane from dp > 4 on (more plans per warp)
 //   2: up to four replicas per lane
+//   3: lane-major kernels (k_lane) for dp <= 32: W = 1/1/2/4 lanes with
+//      R = 4/8/8/8 replicas per lane
 static int g_pack = 0;
-void set_k4_pack(int p) { g_pack = p < 0 ? 0 : (p > 2 ? 2 : p); }
+void set_k4_pack(int p) { g_pack = p < 0 ? 0 : (p > 3 ? 3 : p); }
 
 void class_shape(int cls, int* W, int* R) {
-    static const int Ws[3][7] = {{4, 8, 16, 32, 32, 32, 32}, {4, 4, 8, 16, 32, 32, 32}, {4, 4, 4, 8, 32, 32, 32}};
-    static const int Rs[3][7] = {{1, 1, 1, 1, 2, 4, 8}, {1, 2, 2, 2, 2, 4, 8}, {1, 2, 4, 4, 2, 4, 8}};
+    static const int Ws[4][7] = {{4, 8, 16, 32, 32, 32, 32}, {4, 4, 8, 16, 32, 32, 32}, {4, 4, 4, 8, 32, 32, 32},
+                                 {1, 1, 2, 4, 32, 32, 32}};
+    static const int Rs[4][7] = {{1, 1, 1, 1, 2, 4, 8}, {1, 2, 2, 2, 2, 4, 8}, {1, 2, 4, 4, 2, 4, 8},
+                                 {4, 8, 8, 8, 2, 4, 8}};
     *W = Ws[g_pack][cls];
     *R = Rs[g_pack][cls];
 }
@@ -933,6 +1446,13 @@ void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t 
             case 4: launch_sim_t<32, 2, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
             case 5: launch_sim_t<32, 4, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
             case 6: launch_sim_t<32, 8, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
+        }
+    } else if (g_pack == 3 && cls <= 3) {
+        switch (cls) {
+            case 0: launch_lane_t<1, 4>(a, sm_count, s, launches, grid_out); return;
+            case 1: launch_lane_t<1, 8>(a, sm_count, s, launches, grid_out); return;
+            case 2: launch_lane_t<2, 8>(a, sm_count, s, launches, grid_out); return;
+            case 3: launch_lane_t<4, 8>(a, sm_count, s, launches, grid_out); return;
         }
     } else {
         switch (cls) {
