@@ -314,7 +314,12 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     TieEntry* ties = E.d_ties.as<TieEntry>(E.tie_cap);
     unsigned long long* tiecnt = E.d_tiecnt.as<unsigned long long>(1);
     unsigned long long* ovf = E.d_ovf.as<unsigned long long>(E.ovf_cap);
-    unsigned long long* ovfcnt = E.d_ovfcnt.as<unsigned long long>(1);
+    // ring overflows are collected per replica-count class (slot 7: seeds,
+    // whose overflows are dropped -- the lists re-visit them) over all waves
+    // and re-run once at the end with global-memory rings
+    const unsigned long long ovf_region = (unsigned long long)E.ovf_cap / 8;
+    unsigned long long* ovfcnt = E.d_ovfcnt.as<unsigned long long>(8);
+    CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8 * 8, x.s));
     unsigned long long* ovfcnt2 = E.d_ovfcnt2.as<unsigned long long>(1);
     unsigned long long* ctrs = E.d_ctrs.as<unsigned long long>(CTR_COUNT);
     unsigned long long* ictr = E.d_ictr.as<unsigned long long>(1);
@@ -369,20 +374,19 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     base.tie_cap = (unsigned long long)E.tie_cap;
     base.ovf = ovf;
     base.ovf_count = ovfcnt;
-    base.ovf_cap = (unsigned long long)E.ovf_cap;
+    base.ovf_cap = ovf_region;
     base.scratch = scratch;
     base.sld = sld;
     base.counters = ctrs;
     base.ring_cap = ring_cap;
 
-    // Runs one packed work list through the class kernel, then the deep-queue
-    // re-runs of its ring overflows.
+    // Runs one packed work list through the class kernel; ring overflows are
+    // appended to the class's overflow region.
     auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
                         const unsigned long long* parts, const unsigned long long* parts2,
                         const unsigned long long* perm) {
         if (nitems == 0) return;
         CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
-        CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8, x.s));
         SimArgs a = base;
         a.items = items;
         a.parts = parts;
@@ -391,24 +395,33 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         a.nitems = nitems;
         a.check_stable = seeds ? 1 : 0;
         a.seeds = seeds ? 1 : 0;
+        const int slot = seeds ? 7 : cls;
+        a.ovf = ovf + (size_t)slot * ovf_region;
+        a.ovf_count = ovfcnt + slot;
         launch_sim(a, cls, SIM_LIST, E.sm_count, x.s, &x.launches, nullptr);
-        unsigned long long novf = 0;
-        x.d2h(&novf, ovfcnt, 8);
+    };
+    // Deep-queue re-runs (rings in global memory, capacity >= n_req) of every
+    // overflowed plan, one launch per class.
+    auto run_overflows = [&]() {
+        unsigned long long novf[8];
+        x.d2h(novf, ovfcnt, sizeof(novf));
         x.sync();
-        if (novf > (unsigned long long)E.ovf_cap) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
-        if (!seeds) x.st.plans_overflow += (long long)novf;
-        if (novf > 0 && !seeds) {  // deep-queue re-runs (rings in global memory, capacity >= n_req)
+        for (int cls = 0; cls < 7; ++cls) {
+            if (novf[cls] == 0) continue;
+            if (novf[cls] > ovf_region) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
+            x.st.plans_overflow += (long long)novf[cls];
             SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
             double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
             CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
             CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
-            SimArgs d = a;
-            d.items = ovf;
+            SimArgs d = base;
+            d.items = ovf + (size_t)cls * ovf_region;
             d.parts = nullptr;
             d.parts2 = nullptr;
             d.perm = nullptr;
-            d.nitems = novf;
+            d.nitems = novf[cls];
             d.ring_global = ring;
+            d.ovf = ovf + (size_t)7 * ovf_region;  // cannot overflow (capacity >= n_req)
             d.ovf_count = ovfcnt2;
             launch_sim(d, cls, SIM_DEEP, E.sm_count, x.s, &x.launches, nullptr);
         }
@@ -503,6 +516,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             }
         }
     }
+    run_overflows();
     CG_CUDA(cudaEventRecord(E.ev[9], x.s));
 
     unsigned long long h_ctr[CTR_COUNT], h_ties = 0;

@@ -395,10 +395,27 @@ __device__ unsigned long long group_kth_largest(const double* __restrict__ buf, 
         const int owner = (__ffs(ob) - 1) - gshift;
         digit = __shfl_sync(gm, digit, owner, W);
         before = __shfl_sync(gm, before, owner, W);
+        const int cnt = *hword<W, CONTIG>(hist, gshift, digit);
         prefix |= (unsigned long long)digit << shift;
         pmask |= dm;
         need -= before;
         __syncwarp(gm);
+        if (byte > 0 && (need == 1 || need == cnt)) {
+            // the answer is the largest (need == 1) or the smallest (need ==
+            // cnt) element under the prefix: one scan instead of more passes
+            const bool want_max = need == 1;
+            unsigned long long best = want_max ? 0ull : ~0ull;
+            for (int i = gl; i < n; i += W) {
+                const unsigned long long k = (unsigned long long)__double_as_longlong(buf[i]);
+                if ((k & pmask) == prefix) best = want_max ? (k > best ? k : best) : (k < best ? k : best);
+            }
+#pragma unroll
+            for (int off = W / 2; off > 0; off >>= 1) {
+                const unsigned long long v = __shfl_xor_sync(gm, best, off, W);
+                best = want_max ? (v > best ? v : best) : (v < best ? v : best);
+            }
+            return best;
+        }
     }
     return prefix;
 }
@@ -855,11 +872,16 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
     // arrivals / outputs of the pair holding step k and of the next pair (prefetched)
     double2 tq = make_double2(0.0, 0.0), oq = tq, tq2 = tq, oq2 = tq;
     double avail[R], nd[R];
+    // W == 1: output tokens of the job at the ring head, loaded one pop ahead
+    // (the lanes' rows differ, so a load at pop time would stall on L2)
+    constexpr bool HO = W == 1;
+    double ho[R];
     unsigned ht[R];  // head | tail << 16 of the waiting-job ring
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         avail[r] = INF;
         nd[r] = INF;
+        ho[r] = 0.0;
         ht[r] = 0;
     }
     unsigned long long steps = 0, full = 0, pruned = 0;
@@ -992,11 +1014,14 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     for (int r = 0; r < R; ++r) {
                         if (dep[r]) {
                             const unsigned h = ht[r] & 0xffffu;
-                            if (h != (ht[r] >> 16)) {  // next waiting job enters service
-                                const int kx = ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane];
+                            const unsigned tl = ht[r] >> 16;
+                            if (h != tl) {  // the head job enters service
+                                const double oh = HO ? ho[r] : Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
                                 nd[r] = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
-                                                  __dmul_rn(Orow[kx], dec_s[r * 32 + lane]));
-                                ht[r] = (ht[r] & 0xffff0000u) | ((h + 1u) & 0xffffu);
+                                                  __dmul_rn(oh, dec_s[r * 32 + lane]));
+                                const unsigned h1 = (h + 1u) & 0xffffu;
+                                ht[r] = (ht[r] & 0xffff0000u) | h1;
+                                if (HO && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
                             } else {
                                 nd[r] = INF;
                             }
@@ -1055,6 +1080,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             if (me) {
                 // idle: the FIFO now holds just this job (lazy reset; H = 0 is
                 // an empty ring).  Busy: the job joins the queue.
+                const bool first = !idle && ((H >> 16) == (H & 0xffffu));  // the ring was empty
                 if (!idle) {
                     ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
                     H += 1u << 16;
@@ -1066,6 +1092,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     if (r == rr) {
                         avail[r] = fin;
                         ht[r] = H;
+                        if (HO && first) ho[r] = o;
                     }
                 ab += soj > U ? 1 : 0;
                 scratch[k] = soj;
