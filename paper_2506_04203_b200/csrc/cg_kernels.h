@@ -162,7 +162,21 @@ struct FilterArgs {
     unsigned long long* list_count;            // [7]
     unsigned long long list_cap;               // per class
     unsigned long long* counters;
+    unsigned long long* pilot;                 // optional [row][N+1]: (estimate20 << 44 | plan) minimum
+    int pilot_only;                            // 1: only the pilot minima (no lists, no counters)
 };
+
+// Pilot lists: the best-estimate plan of every (row, budget) cell, by class.
+struct PilotArgs {
+    long long cells;
+    int N;
+    const unsigned long long* pilot;
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    unsigned long long* lists[7];
+    unsigned long long* list_count;            // [7]
+};
+void launch_pilot_lists(const PilotArgs& a, cudaStream_t s, int* launches);
 
 struct SimGeometry {
     int W, R, G, grid;

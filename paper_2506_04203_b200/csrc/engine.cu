@@ -152,6 +152,7 @@ struct cg_engine {
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
+    int pilot = 1;      // pilot plans per (row, budget) cell before each wave's lists (option pilot)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
@@ -166,7 +167,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pcount, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -470,6 +471,52 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned long long* tv = E.d_lv1.as<unsigned long long>(cap);
         unsigned int* rsh = E.d_rshist.as<unsigned int>(radix_hist_entries((long long)cap));
         unsigned long long* lcount = E.d_lcount.as<unsigned long long>(7);
+        // pilot: the best-estimate stable plan of every (row, budget) cell
+        const bool use_pilot = E.pilot && E.prune;
+        unsigned long long* pilot = use_pilot ? E.d_pilot.as<unsigned long long>(cells) : nullptr;
+        unsigned long long* plists = use_pilot ? E.d_plists.as<unsigned long long>((size_t)7 * cells) : nullptr;
+        unsigned long long* pcount = E.d_pcount.as<unsigned long long>(7);
+        if (use_pilot && c_hi > c_lo) {
+            // Pilot: one enumeration of this rank's plans finds, per (row,
+            // budget) cell, the stable plan with the best heuristic estimate;
+            // those are simulated first (one launch for dp <= 32) so the exact
+            // bounds are tight before the bulk lists run.
+            x.fill(pilot, cells, ~0ull);
+            FilterArgs fp{};
+            fp.N = N;
+            fp.n_req = n_req;
+            fp.kstar = kstar;
+            fp.prune = E.prune;
+            fp.nrows = (int)prow.size();
+            fp.row_ids = rowids;
+            fp.chunk_prefix = cpre;
+            fp.chunk_base = c_lo;
+            fp.nchunks = c_hi - c_lo;
+            fp.chunk = chunk;
+            fp.rows = base.rows;
+            fp.spaces = base.spaces;
+            fp.tab = tab;
+            fp.ub = ub;
+            fp.counters = ctrs;
+            fp.pilot = pilot;
+            fp.pilot_only = 1;
+            launch_plan_filter(fp, x.s, &x.launches);
+            CG_CUDA(cudaMemsetAsync(pcount, 0, 7 * 8, x.s));
+            PilotArgs pa{};
+            pa.cells = cells;
+            pa.N = N;
+            pa.pilot = pilot;
+            pa.rows = base.rows;
+            pa.spaces = base.spaces;
+            for (int c = 0; c < 7; ++c) pa.lists[c] = plists + (size_t)c * cells;
+            pa.list_count = pcount;
+            launch_pilot_lists(pa, x.s, &x.launches);
+            unsigned long long pcounts[7];
+            x.d2h(pcounts, pcount, sizeof(pcounts));
+            x.sync();
+            for (int c = 6; c >= 3; --c)
+                run_list(plists + (size_t)c * cells, pcounts[c], c, true, nullptr, nullptr, nullptr);
+        }
         for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
             const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);
             CG_CUDA(cudaMemsetAsync(lcount, 0, 7 * 8, x.s));
@@ -1347,6 +1394,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
+        else if (k == "pilot") e->pilot = (int)value;
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);

@@ -1358,7 +1358,17 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                         ++skipped;
                     }
                 }
-                if (keep) cls = class_of_dp(dp);
+                if (keep && !a.pilot_only) cls = class_of_dp(dp);
+                if (keep && a.pilot) {
+                    // heuristic p95 estimate (order only): service bound / (1 - utilisation)
+                    const double rho = rd.rate / capacity;
+                    double est = lb / (1.0 - rho);
+                    est = est > 0.0 ? est : 0.0;
+                    const unsigned long long v =
+                        (((unsigned long long)__double_as_longlong(est) >> 44) << kItemPlanBits) | p;
+                    unsigned long long* cell = &a.pilot[(long long)row * (a.N + 1) + used];
+                    if (v < *(volatile unsigned long long*)cell) atomicMin(cell, v);
+                }
             }
         }
         // warp-aggregated append into the class lists
@@ -1382,8 +1392,27 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
             }
         }
     }
+    if (a.pilot_only) return;
     if (stable) atomicAdd(&a.counters[CTR_STABLE], stable);
     if (skipped) atomicAdd(&a.counters[CTR_BOUND], skipped);
+}
+
+__global__ void k_pilot_lists(PilotArgs a) {
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= a.cells) return;
+    const unsigned long long v = a.pilot[c];
+    if (v == ~0ull) return;
+    const int row = (int)(c / (a.N + 1));
+    const unsigned long long plan = v & kItemPlanMask;
+    const PlanSpace& sp = a.spaces[a.rows[row].space];
+    unsigned char cn[kMaxShapes];
+    unrank_plan(sp, plan, cn);
+    int dp = 0;
+    for (int s = 0; s < sp.S; ++s) dp += cn[s];
+    int cls = class_of_dp(dp);
+    cls = cls < 3 ? 3 : cls;  // one launch for every plan with dp <= 32 (class 3 covers them)
+    const unsigned long long slot = atomicAdd(&a.list_count[cls], 1ull);
+    a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | plan;
 }
 
 template <int W, int R, int MODE>
@@ -1504,6 +1533,13 @@ void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t 
         }
     }
     throw EngineError(101, "unsupported JSQ kernel class");
+}
+
+void launch_pilot_lists(const PilotArgs& a, cudaStream_t s, int* launches) {
+    if (a.cells == 0) return;
+    k_pilot_lists<<<(unsigned)((a.cells + 127) / 128), 128, 0, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
 }
 
 void launch_plan_filter(const FilterArgs& a, cudaStream_t s, int* launches) {
