@@ -330,7 +330,7 @@ def run_ours(args):
                          "frac": k1_gbs / peak if peak else None, "traffic": committed_k1_traffic(),
                          "peak_kind": peak_kind, "bytes_per_launch": k1_bytes, "ms_per_launch": k1_ms,
                          "bytes_per_request": "16*C+8 (scores of C-1 threshold stages, input, C outputs, 8 B ranks)"},
-            "roofline_k4": {"bound": "issue", "kernel": "k_sim (K4 JSQ simulation)", "ms_per_sweep": k4_ms,
+            "roofline_k4": {"bound": "issue", "kernel": "k_lane / k_sim (K4 JSQ simulation)", "ms_per_sweep": k4_ms,
                             "request_steps_per_s": steps_k4 / (k4_ms / 1000.0) if k4_ms > 0 else None,
                             "plans_simulated_full": st_dev[-1]["plans_simulated_full"],
                             "plans_pruned": st_dev[-1]["plans_pruned"],

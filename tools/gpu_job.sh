@@ -16,8 +16,18 @@ fi
 if [[ $what == *ncu* ]]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv \
       python tools/perf_probe.py C2 - 1 > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_sim -c 8 \
+  timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_(lane|sim)<" -c 16 \
       -o gpurun_out/prof_k4_c2 -f python tools/perf_probe.py C2 - 1 1 > gpurun_out/ncu_k4.log 2>&1; echo "ncu k4 rc=$?"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_route_(tma|hist|tile|aggregate)" -s 1 -c 1 \
       -o gpurun_out/prof_k1_c5 -f python tools/k1_probe.py C5 3 > gpurun_out/ncu_k1.log 2>&1; echo "ncu k1 rc=$?"
+fi
+if [[ $what == *ncu* ]]; then
+  # summarise on the box; full-set reports with source can exceed gpurun's copy-back limit
+  python tools/summarize_ncu.py --launches gpurun_out/launches_c2.csv gpurun_out/launches_c2.json > /dev/null
+  python tools/summarize_ncu.py gpurun_out/prof_k4_c2.ncu-rep gpurun_out/k4_c2_ncu.json > /dev/null
+  python tools/summarize_ncu.py --k4 gpurun_out/prof_k4_c2.ncu-rep gpurun_out/k4_ncu_summary.json \
+      "ncu --set full --clock-control none -k regex:k_(lane|sim)< -c 16 python tools/perf_probe.py C2 - 1 1" > /dev/null
+  python tools/summarize_ncu.py gpurun_out/prof_k1_c5.ncu-rep gpurun_out/k1_c5_ncu.json > /dev/null
+  for f in gpurun_out/*.ncu-rep; do [ $(stat -c %s "$f") -gt 20000000 ] && rm -f "$f"; done
+  du -sh gpurun_out
 fi

@@ -2,6 +2,7 @@
 
   python tools/summarize_ncu.py report.ncu-rep out.json
   python tools/summarize_ncu.py --launches launches.csv out.json
+  python tools/summarize_ncu.py --k4 report.ncu-rep out.json "<source>"   (time-weighted K4 issue summary)
 """
 import csv
 import io
@@ -64,8 +65,25 @@ def launches(path):
                         for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])}}
 
 
+def k4_summary(path, source):
+    """Issue / warps-active utilisation of the captured K4 launches, weighted by duration."""
+    ks = report(path)
+    tw = iw = ww = 0.0
+    for k in ks:
+        t = float(k["gpu__time_duration.sum"].split()[0].replace(",", ""))
+        tw += t
+        iw += t * float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])
+        ww += t * float(k["sm__warps_active.avg.pct_of_peak_sustained_active"].split()[0])
+    return {"source": source, "kernels_captured": len(ks),
+            "issue_active_pct_time_weighted": round(iw / tw, 2) if tw else None,
+            "warps_active_pct_time_weighted": round(ww / tw, 2) if tw else None}
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "--launches":
+    if sys.argv[1] == "--k4":
+        res = k4_summary(sys.argv[2], sys.argv[4] if len(sys.argv) > 4 else sys.argv[2])
+        dst = sys.argv[3]
+    elif sys.argv[1] == "--launches":
         res = launches(sys.argv[2])
         dst = sys.argv[3]
     else:
