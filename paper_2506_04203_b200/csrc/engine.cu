@@ -432,8 +432,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     // Bound seeding: homogeneous plans (c replicas of one shape) of the heavy
     // rows first, so the exact bounds are tight from the start.  Seeds are
     // re-visited by the filtered lists (idempotent), so this only moves work.
+    // With the pilot pass on, the seeds run in the pilot launch instead.
+    std::vector<unsigned long long> seeds;
+    const bool use_pilot = E.pilot && E.prune && !prow.empty();
     if (E.prune && E.world == 1) {
-        std::vector<unsigned long long> seeds;
         for (int r = 0; r < nrows; ++r) {
             const auto& sp = hs[rows[r].space];
             if (sp.num_plans < 4096 || N < 1) continue;
@@ -445,7 +447,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     seeds.push_back(((unsigned long long)r << kItemPlanBits) | (q - 1));
                 }
         }
-        if (!seeds.empty()) {
+        if (!seeds.empty() && !use_pilot) {
             unsigned long long* dseeds = E.d_seeds.as<unsigned long long>(seeds.size());
             x.h2d(dseeds, seeds.data(), seeds.size() * 8);
             run_list(dseeds, seeds.size(), 3, true, nullptr, nullptr, nullptr);
@@ -472,11 +474,11 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned int* rsh = E.d_rshist.as<unsigned int>(radix_hist_entries((long long)cap));
         unsigned long long* lcount = E.d_lcount.as<unsigned long long>(7);
         // pilot: the best-estimate stable plan of every (row, budget) cell
-        const bool use_pilot = E.pilot && E.prune;
+        const size_t pregion = (size_t)cells + seeds.size();  // per-class pilot list capacity
         unsigned long long* pilot = use_pilot ? E.d_pilot.as<unsigned long long>(cells) : nullptr;
-        unsigned long long* plists = use_pilot ? E.d_plists.as<unsigned long long>((size_t)7 * cells) : nullptr;
+        unsigned long long* plists = use_pilot ? E.d_plists.as<unsigned long long>(7 * pregion) : nullptr;
         unsigned long long* pcount = E.d_pcount.as<unsigned long long>(7);
-        if (use_pilot && c_hi > c_lo) {
+        if (use_pilot) {
             // Pilot: one enumeration of this rank's plans finds, per (row,
             // budget) cell, the stable plan with the best heuristic estimate;
             // those are simulated first (one launch for dp <= 32) so the exact
@@ -501,21 +503,24 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fp.pilot = pilot;
             fp.pilot_only = 1;
             launch_plan_filter(fp, x.s, &x.launches);
-            CG_CUDA(cudaMemsetAsync(pcount, 0, 7 * 8, x.s));
+            // the seeds lead the class-3 pilot list (dp <= 32)
+            const unsigned long long pc0[7] = {0, 0, 0, (unsigned long long)seeds.size(), 0, 0, 0};
+            x.h2d(pcount, pc0, sizeof(pc0));
+            if (!seeds.empty()) x.h2d(plists + 3 * pregion, seeds.data(), seeds.size() * 8);
             PilotArgs pa{};
             pa.cells = cells;
             pa.N = N;
             pa.pilot = pilot;
             pa.rows = base.rows;
             pa.spaces = base.spaces;
-            for (int c = 0; c < 7; ++c) pa.lists[c] = plists + (size_t)c * cells;
+            for (int c = 0; c < 7; ++c) pa.lists[c] = plists + (size_t)c * pregion;
             pa.list_count = pcount;
             launch_pilot_lists(pa, x.s, &x.launches);
             unsigned long long pcounts[7];
             x.d2h(pcounts, pcount, sizeof(pcounts));
             x.sync();
             for (int c = 6; c >= 3; --c)
-                run_list(plists + (size_t)c * cells, pcounts[c], c, true, nullptr, nullptr, nullptr);
+                run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, nullptr);
         }
         for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
             const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);

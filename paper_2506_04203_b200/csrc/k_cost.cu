@@ -989,7 +989,10 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             }
             const bool busy = run && !idle;
             int rr = __ffs(m) - 1;
-            double A = t;  // start time: t when a replica is idle, else avail of the chosen one
+            // the idle candidate's finish (start = t), issued before the busy
+            // block so its shared-memory loads and fp64 chain overlap it
+            const int pidx0 = (rr > 0 ? rr : 0) * 32 + lane;
+            double fin = __dadd_rn(__dadd_rn(t, pre_s[pidx0]), __dmul_rn(o, dec_s[pidx0]));
             unsigned H = 0;
             if (__any_sync(FULL, busy)) {
                 if (busy && lazy) {
@@ -1069,13 +1072,13 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                             hv[r] = hi ? hv[r + w] : hv[r];
                         }
                     }
-                    A = av[0];  // > t: std::max(t, avail)
                     H = hv[0];
+                    // start = avail of the chosen replica (> t: std::max(t, avail))
+                    const int pidx = rr * 32 + lane;
+                    fin = __dadd_rn(__dadd_rn(av[0], pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
                 }
             }
             const bool me = run && gl == wlane;
-            const int pidx = (me ? rr : 0) * 32 + lane;
-            const double fin = __dadd_rn(__dadd_rn(A, pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
             const double soj = __dsub_rn(fin, t);
             if (me) {
                 // idle: the FIFO now holds just this job (lazy reset; H = 0 is
