@@ -831,6 +831,8 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
     return true;
 }
 
+constexpr unsigned kLaneCheck = 32;  // request-steps between exact-bound prune checks
+
 template <int W, int R>
 __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
     using TR = LaneTraits<W, R>;
@@ -1120,7 +1122,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
-        if ((it & (32u / UNROLL - 1u)) == (32u / UNROLL - 1u)) {
+        if ((it & (kLaneCheck / UNROLL - 1u)) == (kLaneCheck / UNROLL - 1u)) {
             int tot = ab;
             int ov = ovf ? 1 : 0;
 #pragma unroll
