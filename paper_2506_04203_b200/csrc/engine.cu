@@ -152,7 +152,8 @@ struct cg_engine {
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
-    int pilot = 1;      // pilot plans per (row, budget) cell before each wave's lists (option pilot)
+    int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
+    int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
@@ -462,7 +463,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         x.h2d(cpre, chunk_prefix.data(), chunk_prefix.size() * 8);
         uint64_t c_lo = 0, c_hi = 0;
         cg_shard_range(chunk_prefix.back(), E.rank, E.world, &c_lo, &c_hi);
-        const unsigned long long wave_chunks = (16ull << 20) / chunk;
+        const unsigned long long wave_chunks = ((unsigned long long)E.wave_plans << 20) / chunk;
         const unsigned long long cap = wave_chunks * chunk;
         unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* lparts = E.d_lparts.as<unsigned long long>((size_t)7 * cap);
@@ -1400,6 +1401,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "pilot") e->pilot = (int)value;
+        else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);
         else if (k == "tie_capacity") e->tie_cap = std::max<int64_t>(16, value);
