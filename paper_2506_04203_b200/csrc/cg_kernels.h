@@ -164,6 +164,7 @@ struct FilterArgs {
     unsigned long long* counters;
     unsigned long long* pilot;                 // optional [row][N+1]: (estimate20 << 44 | plan) minimum
     int pilot_only;                            // 1: only the pilot minima (no lists, no counters)
+    unsigned long long pilot_min_plans;        // rows with fewer plans get no pilot
 };
 
 // Pilot lists: the best-estimate plan of every (row, budget) cell, by class.
@@ -175,6 +176,7 @@ struct PilotArgs {
     const PlanSpace* spaces;
     unsigned long long* lists[7];
     unsigned long long* list_count;            // [7]
+    int merge;                                 // 0: native classes, 1: class 0 + {1,2,3} -> 3, 2: {0..3} -> 3
 };
 void launch_pilot_lists(const PilotArgs& a, cudaStream_t s, int* launches);
 

@@ -153,6 +153,8 @@ struct cg_engine {
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
+    long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
+    int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
@@ -503,6 +505,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fp.counters = ctrs;
             fp.pilot = pilot;
             fp.pilot_only = 1;
+            fp.pilot_min_plans = (unsigned long long)E.pilot_min_plans;
             launch_plan_filter(fp, x.s, &x.launches);
             // the seeds lead the class-3 pilot list (dp <= 32)
             const unsigned long long pc0[7] = {0, 0, 0, (unsigned long long)seeds.size(), 0, 0, 0};
@@ -516,11 +519,12 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             pa.spaces = base.spaces;
             for (int c = 0; c < 7; ++c) pa.lists[c] = plists + (size_t)c * pregion;
             pa.list_count = pcount;
+            pa.merge = E.pilot_merge;
             launch_pilot_lists(pa, x.s, &x.launches);
             unsigned long long pcounts[7];
             x.d2h(pcounts, pcount, sizeof(pcounts));
             x.sync();
-            for (int c = 6; c >= 3; --c)
+            for (int c = 6; c >= 0; --c)
                 run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, nullptr);
         }
         for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
@@ -1401,6 +1405,8 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "pilot") e->pilot = (int)value;
+        else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
+        else if (k == "pilot_merge") e->pilot_merge = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
         else if (k == "overflow_capacity") e->ovf_cap = std::max<int64_t>(16, value);

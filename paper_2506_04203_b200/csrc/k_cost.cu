@@ -1364,7 +1364,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                     }
                 }
                 if (keep && !a.pilot_only) cls = class_of_dp(dp);
-                if (keep && a.pilot) {
+                if (keep && a.pilot && sp.num_plans >= a.pilot_min_plans) {
                     // heuristic p95 estimate (order only): service bound / (1 - utilisation)
                     const double rho = rd.rate / capacity;
                     double est = lb / (1.0 - rho);
@@ -1415,7 +1415,9 @@ __global__ void k_pilot_lists(PilotArgs a) {
     int dp = 0;
     for (int s = 0; s < sp.S; ++s) dp += cn[s];
     int cls = class_of_dp(dp);
-    cls = cls < 3 ? 3 : cls;  // one launch for every plan with dp <= 32 (class 3 covers them)
+    // fewer, larger launches: class 3's kernel covers every dp <= 32
+    if (a.merge == 2 && cls < 3) cls = 3;
+    if (a.merge == 1 && cls >= 1 && cls < 3) cls = 3;
     const unsigned long long slot = atomicAdd(&a.list_count[cls], 1ull);
     a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | plan;
 }
