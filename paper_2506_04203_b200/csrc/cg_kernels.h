@@ -165,6 +165,7 @@ struct FilterArgs {
     unsigned long long* pilot;                 // optional [row][N+1]: (estimate20 << 44 | plan) minimum
     int pilot_only;                            // 1: only the pilot minima (no lists, no counters)
     unsigned long long pilot_min_plans;        // rows with fewer plans get no pilot
+    int sort_key;                              // list order: 0 service bound, 1 estimate
 };
 
 // Pilot lists: the best-estimate plan of every (row, budget) cell, by class.

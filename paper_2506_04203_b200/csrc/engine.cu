@@ -155,6 +155,7 @@ struct cg_engine {
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
+    int sort_key = 1;   // bulk list order (option sort_key): 0 service bound, 1 estimate
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
@@ -554,6 +555,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fa.list_count = lcount;
             fa.list_cap = cap;
             fa.counters = ctrs;
+            fa.sort_key = E.sort_key;
             launch_plan_filter(fa, x.s, &x.launches);
             unsigned long long counts[7];
             x.d2h(counts, lcount, sizeof(counts));
@@ -1405,6 +1407,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "pilot") e->pilot = (int)value;
+        else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
         else if (k == "pilot_merge") e->pilot_merge = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));

@@ -1354,7 +1354,14 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 ++stable;
                 bool keep = true;
                 lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
-                key = dbl_to_key(lb) >> 48;  // coarse order key: likely-good plans first
+                // coarse order key, likely-good plans first: the service bound,
+                // or (sort_key 1) the heuristic estimate service bound / (1 - utilisation)
+                double kv = lb;
+                if (a.sort_key == 1) {
+                    const double est = lb / (1.0 - rd.rate / capacity);
+                    kv = est > 0.0 ? est : 0.0;
+                }
+                key = dbl_to_key(kv) >> 48;
                 if (a.prune) {
                     const double U = __longlong_as_double(
                         (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
