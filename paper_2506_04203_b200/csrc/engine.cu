@@ -155,7 +155,8 @@ struct cg_engine {
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
-    int sort_key = 1;   // bulk list order (option sort_key): 0 service bound, 1 estimate
+    int sort_key = 3;   // list/pilot order (option sort_key): 0 service bound, else an estimate (k_plan_filter)
+    int class_order = 1;  // 0: lists by replica count descending, 1: ascending (option class_order)
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
@@ -507,6 +508,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fp.pilot = pilot;
             fp.pilot_only = 1;
             fp.pilot_min_plans = (unsigned long long)E.pilot_min_plans;
+            fp.sort_key = E.sort_key ? E.sort_key : 1;
             launch_plan_filter(fp, x.s, &x.launches);
             // the seeds lead the class-3 pilot list (dp <= 32)
             const unsigned long long pc0[7] = {0, 0, 0, (unsigned long long)seeds.size(), 0, 0, 0};
@@ -560,7 +562,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             unsigned long long counts[7];
             x.d2h(counts, lcount, sizeof(counts));
             x.sync();
-            for (int c = 6; c >= 0; --c) {
+            for (int ci = 0; ci < 7; ++ci) {
+                const int c = E.class_order ? ci : 6 - ci;
                 unsigned long long* items = lists + (size_t)c * cap;
                 const unsigned long long* perm = nullptr;
                 if (E.prune && counts[c] > 1) {  // ascending service bound (16-bit key: 2 passes) of slot indices
@@ -1408,6 +1411,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "pilot") e->pilot = (int)value;
         else if (k == "sort_key") e->sort_key = (int)value;
+        else if (k == "class_order") e->class_order = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
         else if (k == "pilot_merge") e->pilot_merge = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));

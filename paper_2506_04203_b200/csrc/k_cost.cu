@@ -1338,7 +1338,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
         unsigned long long key = 0;
         if (live) {
             bool good = true;
-            double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll);
+            double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll), slow = 0.0;
             for (int s = 0; s < sp.S; ++s) {
                 const int cnt = c[s];
                 if (!cnt) continue;
@@ -1349,6 +1349,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 capacity = __dadd_rn(capacity, __ddiv_rn((double)cnt, a.tab.mean_service[rb + s]));
                 const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
                 lb = v < lb ? v : lb;
+                slow = v > slow ? v : slow;
             }
             if (good && rd.rate < capacity) {
                 ++stable;
@@ -1356,12 +1357,19 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
                 // coarse order key, likely-good plans first: the service bound,
                 // or (sort_key 1) the heuristic estimate service bound / (1 - utilisation)
-                double kv = lb;
-                if (a.sort_key == 1) {
-                    const double est = lb / (1.0 - rd.rate / capacity);
-                    kv = est > 0.0 ? est : 0.0;
-                }
-                key = dbl_to_key(kv) >> 48;
+                // order heuristics (results never depend on them): 1 fast-shape
+                // bound / (1 - rho), 3 (default) mean of the fastest and slowest
+                // shapes' bounds / (1 - rho), ...
+                const double rho = rd.rate / capacity;
+                double est = lb;
+                if (a.sort_key == 1) est = lb / (1.0 - rho);
+                else if (a.sort_key == 2) est = lb / ((1.0 - rho) * (1.0 - rho));
+                else if (a.sort_key == 3) est = 0.5 * (lb + slow) / (1.0 - rho);
+                else if (a.sort_key == 4) est = slow / (1.0 - rho);
+                else if (a.sort_key == 5) est = 0.25 * (lb + 3.0 * slow) / (1.0 - rho);
+                else if (a.sort_key == 6) est = slow / ((1.0 - rho) * (1.0 - rho));
+                est = est > 0.0 ? est : 0.0;
+                key = dbl_to_key(a.sort_key ? est : lb) >> 48;
                 if (a.prune) {
                     const double U = __longlong_as_double(
                         (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
@@ -1373,9 +1381,6 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 if (keep && !a.pilot_only) cls = class_of_dp(dp);
                 if (keep && a.pilot && sp.num_plans >= a.pilot_min_plans) {
                     // heuristic p95 estimate (order only): service bound / (1 - utilisation)
-                    const double rho = rd.rate / capacity;
-                    double est = lb / (1.0 - rho);
-                    est = est > 0.0 ? est : 0.0;
                     const unsigned long long v =
                         (((unsigned long long)__double_as_longlong(est) >> 44) << kItemPlanBits) | p;
                     unsigned long long* cell = &a.pilot[(long long)row * (a.N + 1) + used];
