@@ -110,6 +110,9 @@ enum : int { CTR_STABLE = 0, CTR_FULL = 1, CTR_PRUNED = 2, CTR_STEPS = 3, CTR_BO
              CTR_COUNT = 8 };
 enum : int { SIM_RANGE = 0, SIM_LIST = 1, SIM_DEEP = 2 };
 
+// Bits of the filter's order key (top bits of the sortable estimate) the lists are sorted by.
+constexpr int kListKeyBits = 16;
+
 // Work items: (row << 44) | plan index.
 constexpr int kItemPlanBits = 44;
 constexpr unsigned long long kItemPlanMask = (1ull << kItemPlanBits) - 1ull;

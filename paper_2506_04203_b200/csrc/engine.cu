@@ -571,7 +571,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     CG_LAUNCH_CHECK();
                     ++x.launches;
                     const int par = radix_sort_u64(lkeys + (size_t)c * cap, tidx, tk, tv, (long long)counts[c],
-                                                   0xffffull, rsh, x.s, &x.launches);
+                                                   (1ull << kListKeyBits) - 1ull, rsh, x.s, &x.launches);
                     perm = par ? tv : tidx;
                 }
                 run_list(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm);

@@ -1369,7 +1369,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 else if (a.sort_key == 5) est = 0.25 * (lb + 3.0 * slow) / (1.0 - rho);
                 else if (a.sort_key == 6) est = slow / ((1.0 - rho) * (1.0 - rho));
                 est = est > 0.0 ? est : 0.0;
-                key = dbl_to_key(a.sort_key ? est : lb) >> 48;
+                key = dbl_to_key(a.sort_key ? est : lb) >> (64 - kListKeyBits);
                 if (a.prune) {
                     const double U = __longlong_as_double(
                         (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
