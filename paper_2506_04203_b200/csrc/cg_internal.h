@@ -51,6 +51,7 @@ struct RowTables {
     double* prefill;
     double* decode;
     double* mean_service;
+    double* inv_service;  // fl(1 / mean_service): the filter's fast stability test
     double* T;            // [row][ld] CRN arrivals (first n_req used)
     double* O;            // [row][ld] CRN outputs
     int ld;               // row stride: n_req rounded up to a multiple of 4 (32-byte rows)

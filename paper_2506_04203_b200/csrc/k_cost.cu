@@ -83,7 +83,7 @@ __global__ void k_row_shapes(RowSetupArgs a) {
     const bool ok = dev_memory_feasible(tp, pp, m, a.hw, a.p, kv_tokens);
     a.tab.shape_ok[o] = ok ? 1 : 0;
     if (!ok) {
-        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = 0.0;
+        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = a.tab.inv_service[o] = 0.0;
         return;
     }
     // service_time (costmodel.cpp:176-194) with the reference's op order
@@ -100,6 +100,7 @@ __global__ void k_row_shapes(RowSetupArgs a) {
     a.tab.prefill[o] = prefill;
     a.tab.decode[o] = decode;
     a.tab.mean_service[o] = __dadd_rn(prefill, __dmul_rn(clamped_mean_out, decode));
+    a.tab.inv_service[o] = __drcp_rn(a.tab.mean_service[o]);
 }
 
 // Common random numbers (costmodel.cpp:331-342).  L[k] = log1p(-u_k) comes
@@ -1337,6 +1338,11 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
         int cls = -1;
         unsigned long long key = 0;
         if (live) {
+            // Stability (costmodel.cpp:366-376): rate < sum over parts of cnt /
+            // mean_service, summed in parts order.  Fast test first: each term
+            // cnt * fl(1/ms) is within 2u(1+u) of cnt/ms and both sums carry at
+            // most S roundings, so the two capacities differ by < 2(S+3)u <
+            // 1e-13 relative; only rates inside that band take the exact path.
             bool good = true;
             double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll), slow = 0.0;
             for (int s = 0; s < sp.S; ++s) {
@@ -1346,12 +1352,19 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                     good = false;
                     break;
                 }
-                capacity = __dadd_rn(capacity, __ddiv_rn((double)cnt, a.tab.mean_service[rb + s]));
+                capacity += (double)cnt * a.tab.inv_service[rb + s];
                 const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
                 lb = v < lb ? v : lb;
                 slow = v > slow ? v : slow;
             }
-            if (good && rd.rate < capacity) {
+            bool stable_plan = good && rd.rate < capacity * (1.0 - 1e-13);
+            if (good && !stable_plan && rd.rate < capacity * (1.0 + 1e-13)) {  // the exact reference sum
+                double exact = 0.0;
+                for (int s = 0; s < sp.S; ++s)
+                    if (c[s]) exact = __dadd_rn(exact, __ddiv_rn((double)c[s], a.tab.mean_service[rb + s]));
+                stable_plan = rd.rate < exact;
+            }
+            if (stable_plan) {
                 ++stable;
                 bool keep = true;
                 lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
