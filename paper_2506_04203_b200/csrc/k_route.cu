@@ -989,7 +989,25 @@ __global__ void __launch_bounds__(QT_THREADS) k_quality(const double* __restrict
             for (int k = threadIdx.x; k < len; k += QT_THREADS)
                 tile[i][k] = scores[(long long)i * n + base + k];
         __syncthreads();
-        for (int k = 0; k < len; ++k) {
+        // accepted scores of 16 requests first (independent of the sum), then
+        // the trace-order chain of 16 adds: the chain is the only serial part
+        constexpr int QB = 16;
+        int k = 0;
+        for (; k + QB <= len; k += QB) {
+            double acc[QB];
+#pragma unroll
+            for (int j = 0; j < QB; ++j) {
+                acc[j] = tile[C - 1][k + j];
+#pragma unroll
+                for (int d = D - 1; d >= 0; --d) {
+                    const double s = tile[d][k + j];
+                    acc[j] = (s >= h[d]) ? s : acc[j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < QB; ++j) sum = __dadd_rn(sum, acc[j]);
+        }
+        for (; k < len; ++k) {
             double acc = tile[C - 1][k];
 #pragma unroll
             for (int d = D - 1; d >= 0; --d) {
