@@ -145,6 +145,7 @@ struct cg_engine {
     int device = 0;
     int sm_count = 148;
     cudaStream_t s = nullptr;
+    cudaStream_t s2 = nullptr;  // second stream: the concurrent pilot launch
     int rank = 0, world = 1;
     cg_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
@@ -329,7 +330,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8 * 8, x.s));
     unsigned long long* ovfcnt2 = E.d_ovfcnt2.as<unsigned long long>(1);
     unsigned long long* ctrs = E.d_ctrs.as<unsigned long long>(CTR_COUNT);
-    unsigned long long* ictr = E.d_ictr.as<unsigned long long>(1);
+    unsigned long long* ictr = E.d_ictr.as<unsigned long long>(2);  // [1]: the concurrent pilot launch
     CG_CUDA(cudaMemsetAsync(tiecnt, 0, 8, x.s));
     CG_CUDA(cudaMemsetAsync(ctrs, 0, 8 * CTR_COUNT, x.s));
 
@@ -360,7 +361,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         max_slots = std::max(max_slots, sim_geometry(cls, SIM_DEEP, E.sm_count).slots);
     }
     const int sld = (n_req + 3) & ~3;  // 32-byte scratch columns
-    double* scratch = E.d_scratch.as<double>((size_t)max_slots * sld);
+    // two scratch regions: the pilot's two launches run concurrently
+    double* scratch = E.d_scratch.as<double>((size_t)2 * max_slots * sld);
     int ring_cap = 1;
     while (ring_cap < n_req) ring_cap <<= 1;
 
@@ -389,12 +391,14 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
 
     // Runs one packed work list through the class kernel; ring overflows are
     // appended to the class's overflow region.
-    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
-                        const unsigned long long* parts, const unsigned long long* parts2,
-                        const unsigned long long* perm) {
+    auto run_list_on = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
+                           const unsigned long long* parts, const unsigned long long* parts2,
+                           const unsigned long long* perm, cudaStream_t st, int region) {
         if (nitems == 0) return;
-        CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
+        CG_CUDA(cudaMemsetAsync(ictr + region, 0, 8, st));
         SimArgs a = base;
+        a.item_counter = ictr + region;
+        a.scratch = scratch + (size_t)region * max_slots * sld;
         a.items = items;
         a.parts = parts;
         a.parts2 = parts2;
@@ -405,7 +409,12 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         const int slot = seeds ? 7 : cls;
         a.ovf = ovf + (size_t)slot * ovf_region;
         a.ovf_count = ovfcnt + slot;
-        launch_sim(a, cls, SIM_LIST, E.sm_count, x.s, &x.launches, nullptr);
+        launch_sim(a, cls, SIM_LIST, E.sm_count, st, &x.launches, nullptr);
+    };
+    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
+                        const unsigned long long* parts, const unsigned long long* parts2,
+                        const unsigned long long* perm) {
+        run_list_on(items, nitems, cls, seeds, parts, parts2, perm, x.s, 0);
     };
     // Deep-queue re-runs (rings in global memory, capacity >= n_req) of every
     // overflowed plan, one launch per class.
@@ -528,8 +537,14 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             unsigned long long pcounts[7];
             x.d2h(pcounts, pcount, sizeof(pcounts));
             x.sync();
-            for (int c = 6; c >= 0; --c)
+            // class 0 (dp <= 4) on the second stream, concurrently with the rest
+            CG_CUDA(cudaEventRecord(E.ev[10], x.s));
+            CG_CUDA(cudaStreamWaitEvent(E.s2, E.ev[10], 0));
+            run_list_on(plists, pcounts[0], 0, true, nullptr, nullptr, nullptr, E.s2, 1);
+            for (int c = 6; c >= 1; --c)
                 run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, nullptr);
+            CG_CUDA(cudaEventRecord(E.ev[11], E.s2));
+            CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
         }
         for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
             const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);
@@ -1374,6 +1389,7 @@ cg_status cg_engine_create(int32_t device, cg_engine** out) {
         e->device = device;
         e->sm_count = prop.multiProcessorCount;
         CG_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
+        CG_CUDA(cudaStreamCreateWithFlags(&e->s2, cudaStreamNonBlocking));
         for (auto& ev : e->ev) CG_CUDA(cudaEventCreate(&ev));
         *out = e;
     });
@@ -1386,6 +1402,7 @@ void cg_engine_destroy(cg_engine* e) {
     cudaSetDevice(e->device);
     for (auto& ev : e->ev) cudaEventDestroy(ev);
     if (e->s) cudaStreamDestroy(e->s);
+    if (e->s2) cudaStreamDestroy(e->s2);
     delete e;
 }
 
