@@ -493,6 +493,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned long long* pilot = use_pilot ? E.d_pilot.as<unsigned long long>(cells) : nullptr;
         unsigned long long* plists = use_pilot ? E.d_plists.as<unsigned long long>(7 * pregion) : nullptr;
         unsigned long long* pcount = E.d_pcount.as<unsigned long long>(7);
+        bool pilot_join = false;
         if (use_pilot) {
             // Pilot: one enumeration of this rank's plans finds, per (row,
             // budget) cell, the stable plan with the best heuristic estimate;
@@ -544,7 +545,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             for (int c = 6; c >= 1; --c)
                 run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, nullptr);
             CG_CUDA(cudaEventRecord(E.ev[11], E.s2));
-            CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
+            pilot_join = true;  // joined before the first bulk list: it overlaps the wave filter
         }
         for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
             const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);
@@ -578,6 +579,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             unsigned long long counts[7];
             x.d2h(counts, lcount, sizeof(counts));
             x.sync();
+            if (pilot_join) {
+                CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
+                pilot_join = false;
+            }
             for (int ci = 0; ci < 7; ++ci) {
                 const int c = E.class_order ? ci : 6 - ci;
                 unsigned long long* items = lists + (size_t)c * cap;
@@ -594,6 +599,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             }
         }
     }
+    CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));  // the pilot's second stream (no-op if unused)
     run_overflows();
     CG_CUDA(cudaEventRecord(E.ev[9], x.s));
 
