@@ -218,7 +218,18 @@ cg_status cg_engine_set_collective(cg_engine* engine, int32_t rank, int32_t worl
 /* The engine's CUDA stream (cudaStream_t): every kernel and copy of a call runs
  * on it, so callers can bracket calls with their own CUDA events. */
 void* cg_engine_stream(cg_engine* engine);
-/* Debug/parity knob: 0 disables the exact p95-bound pruning in K4. */
+/* Engine options.  None changes any result (tests/test_gpu_parity.py checks
+ * each); they select work order and kernel forms:
+ *   "prune"            1 (default) exact p95-bound elimination in K4; 0 simulates every stable plan
+ *   "k4_pack"          3 (default) lane-major k_lane for dp <= 32; 0-2 group-per-plan k_sim forms
+ *   "pilot"            1 (default) best-estimate plan per (row, budget) simulated first
+ *   "pilot_merge"      1 (default) pilot launch grouping (0 per class, 2 one launch)
+ *   "pilot_min_plans"  0 (default) rows with fewer plans get no pilot
+ *   "sort_key"         3 (default) work-list order estimate (0 raw service bound)
+ *   "class_order"      1 (default) replica-count classes ascending (0 descending)
+ *   "wave_plans"       64 (default) plans per filter wave in units of 2^20 (~248 B of HBM per plan)
+ *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle" (diagnostic)
+ * Unknown keys return CG_ERR_INVALID_INPUT. */
 cg_status cg_engine_set_option(cg_engine* engine, const char* key, int64_t value);
 
 cg_status cg_sweep(cg_engine* engine, const cg_trace* trace, const cg_model* models,
