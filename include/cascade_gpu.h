@@ -225,6 +225,7 @@ void* cg_engine_stream(cg_engine* engine);
  *   "pilot"            1 (default) best-estimate plan per (row, budget) simulated first
  *   "pilot_merge"      1 (default) pilot launch grouping (0 per class, 2 one launch)
  *   "pilot_min_plans"  0 (default) rows with fewer plans get no pilot
+ *   "pilot_sort"       1 (default) pilot lists in ascending estimate order
  *   "sort_key"         3 (default) work-list order estimate (0 raw service bound)
  *   "class_order"      1 (default) replica-count classes ascending (0 descending)
  *   "wave_plans"       64 (default) plans per filter wave in units of 2^20 (~248 B of HBM per plan)

@@ -179,6 +179,7 @@ struct PilotArgs {
     const RowDesc* rows;
     const PlanSpace* spaces;
     unsigned long long* lists[7];
+    unsigned long long* keys[7];               // the items' estimate (order key)
     unsigned long long* list_count;            // [7]
     int merge;                                 // 0: native classes, 1: class 0 + {1,2,3} -> 3, 2: {0..3} -> 3
 };

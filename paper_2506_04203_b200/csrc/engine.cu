@@ -156,6 +156,7 @@ struct cg_engine {
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
+    int pilot_sort = 1;             // pilot lists in ascending estimate order (option pilot_sort)
     int sort_key = 3;   // list/pilot order (option sort_key): 0 service bound, else an estimate (k_plan_filter)
     int class_order = 1;  // 0: lists by replica count descending, 1: ascending (option class_order)
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
@@ -173,7 +174,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pcount, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -492,6 +493,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         const size_t pregion = (size_t)cells + seeds.size();  // per-class pilot list capacity
         unsigned long long* pilot = use_pilot ? E.d_pilot.as<unsigned long long>(cells) : nullptr;
         unsigned long long* plists = use_pilot ? E.d_plists.as<unsigned long long>(7 * pregion) : nullptr;
+        unsigned long long* pkeys = use_pilot ? E.d_pkeys.as<unsigned long long>(7 * pregion) : nullptr;
+        unsigned long long* ptk = use_pilot ? E.d_ptk.as<unsigned long long>(pregion) : nullptr;
+        unsigned long long* ptv = use_pilot ? E.d_ptv.as<unsigned long long>(pregion) : nullptr;
+        unsigned int* prsh = use_pilot ? E.d_prsh.as<unsigned int>(radix_hist_entries((long long)pregion)) : nullptr;
         unsigned long long* pcount = E.d_pcount.as<unsigned long long>(7);
         bool pilot_join = false;
         if (use_pilot) {
@@ -524,26 +529,47 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             // the seeds lead the class-3 pilot list (dp <= 32)
             const unsigned long long pc0[7] = {0, 0, 0, (unsigned long long)seeds.size(), 0, 0, 0};
             x.h2d(pcount, pc0, sizeof(pc0));
-            if (!seeds.empty()) x.h2d(plists + 3 * pregion, seeds.data(), seeds.size() * 8);
+            if (!seeds.empty()) {
+                x.h2d(plists + 3 * pregion, seeds.data(), seeds.size() * 8);
+                CG_CUDA(cudaMemsetAsync(pkeys + 3 * pregion, 0, seeds.size() * 8, x.s));
+            }
             PilotArgs pa{};
             pa.cells = cells;
             pa.N = N;
             pa.pilot = pilot;
             pa.rows = base.rows;
             pa.spaces = base.spaces;
-            for (int c = 0; c < 7; ++c) pa.lists[c] = plists + (size_t)c * pregion;
+            for (int c = 0; c < 7; ++c) {
+                pa.lists[c] = plists + (size_t)c * pregion;
+                pa.keys[c] = pkeys + (size_t)c * pregion;
+            }
             pa.list_count = pcount;
             pa.merge = E.pilot_merge;
             launch_pilot_lists(pa, x.s, &x.launches);
             unsigned long long pcounts[7];
             x.d2h(pcounts, pcount, sizeof(pcounts));
             x.sync();
+            // each class list in ascending estimate order (seeds first): pilots of
+            // a row then prune against the row's better cells already done
+            const unsigned long long* pperm[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+            unsigned long long* permbuf = E.d_pperm.as<unsigned long long>(7 * pregion);
+            for (int c = 0; c < 7; ++c) {
+                if (pcounts[c] < 2 || !E.pilot_sort) continue;
+                unsigned long long* pi = permbuf + (size_t)c * pregion;
+                k_iota_u64<<<(unsigned)((pcounts[c] + 255) / 256), 256, 0, x.s>>>(pi, (long long)pcounts[c]);
+                CG_LAUNCH_CHECK();
+                ++x.launches;
+                const int par = radix_sort_u64(pkeys + (size_t)c * pregion, pi, ptk, ptv, (long long)pcounts[c],
+                                               (1ull << 21) - 1ull, prsh, x.s, &x.launches);
+                if (par) CG_CUDA(cudaMemcpyAsync(pi, ptv, pcounts[c] * 8, cudaMemcpyDeviceToDevice, x.s));
+                pperm[c] = pi;
+            }
             // class 0 (dp <= 4) on the second stream, concurrently with the rest
             CG_CUDA(cudaEventRecord(E.ev[10], x.s));
             CG_CUDA(cudaStreamWaitEvent(E.s2, E.ev[10], 0));
-            run_list_on(plists, pcounts[0], 0, true, nullptr, nullptr, nullptr, E.s2, 1);
+            run_list_on(plists, pcounts[0], 0, true, nullptr, nullptr, pperm[0], E.s2, 1);
             for (int c = 6; c >= 1; --c)
-                run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, nullptr);
+                run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, pperm[c]);
             CG_CUDA(cudaEventRecord(E.ev[11], E.s2));
             pilot_join = true;  // joined before the first bulk list: it overlaps the wave filter
         }
@@ -1437,6 +1463,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "class_order") e->class_order = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
+        else if (k == "pilot_sort") e->pilot_sort = (int)value;
         else if (k == "pilot_merge") e->pilot_merge = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);

@@ -1445,6 +1445,7 @@ __global__ void k_pilot_lists(PilotArgs a) {
     if (a.merge == 1 && cls >= 1 && cls < 3) cls = 3;
     const unsigned long long slot = atomicAdd(&a.list_count[cls], 1ull);
     a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | plan;
+    a.keys[cls][slot] = 1ull + (v >> kItemPlanBits);  // 20-bit estimate + 1 (seeds carry key 0)
 }
 
 template <int W, int R, int MODE>
