@@ -478,7 +478,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         x.h2d(cpre, chunk_prefix.data(), chunk_prefix.size() * 8);
         uint64_t c_lo = 0, c_hi = 0;
         cg_shard_range(chunk_prefix.back(), E.rank, E.world, &c_lo, &c_hi);
-        const unsigned long long wave_chunks = ((unsigned long long)E.wave_plans << 20) / chunk;
+        // list capacity: one wave, but never more than this rank's plans
+        const unsigned long long wave_chunks =
+            std::max<unsigned long long>(1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk,
+                                                                         c_hi - c_lo));
         const unsigned long long cap = wave_chunks * chunk;
         unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* lparts = E.d_lparts.as<unsigned long long>((size_t)7 * cap);
