@@ -1323,9 +1323,13 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
     const long long rb = (long long)row * kMaxShapes;
     unsigned char c[kMaxShapes];
     int used = 0, dp = 0;
+    unsigned nz = 0;  // bit s: c[s] > 0 (the loops below visit the plan's parts only)
     if (active) {
         used = unrank_plan(sp, lo, c);
-        for (int s = 0; s < sp.S; ++s) dp += c[s];
+        for (int s = 0; s < sp.S; ++s) {
+            dp += c[s];
+            nz |= c[s] ? (1u << s) : 0u;
+        }
     }
     const double o_k = active ? a.tab.O[(long long)row * a.tab.ld + a.kstar] : 0.0;
     const double t_max = active ? a.tab.T[(long long)row * a.tab.ld + a.n_req - 1] : 0.0;
@@ -1334,7 +1338,23 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
     for (unsigned long long k = 0; k < trips; ++k) {
         const unsigned long long p = lo + k;
         const bool live = active && p < hi;
-        if (live && k > 0) next_plan(sp, c, used, dp);
+        if (live && k > 0) {
+            // lexicographic successor (plan_dev.cuh next_plan) keeping nz
+            for (int i = sp.S - 1; i >= 0; --i) {
+                const int size = sp.shapes[i].gpus;
+                if (used + size <= sp.N) {
+                    c[i] = (unsigned char)(c[i] + 1);
+                    used += size;
+                    dp += 1;
+                    nz |= 1u << i;
+                    break;
+                }
+                used -= c[i] * size;
+                dp -= c[i];
+                c[i] = 0;
+                nz &= ~(1u << i);
+            }
+        }
         int cls = -1;
         unsigned long long key = 0;
         if (live) {
@@ -1345,9 +1365,9 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
             // 1e-13 relative; only rates inside that band take the exact path.
             bool good = true;
             double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll), slow = 0.0;
-            for (int s = 0; s < sp.S; ++s) {
+            for (unsigned m = nz; m; m &= m - 1u) {
+                const int s = __ffs(m) - 1;
                 const int cnt = c[s];
-                if (!cnt) continue;
                 if (!a.tab.shape_ok[rb + s]) {
                     good = false;
                     break;
@@ -1360,8 +1380,10 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
             bool stable_plan = good && rd.rate < capacity * (1.0 - 1e-13);
             if (good && !stable_plan && rd.rate < capacity * (1.0 + 1e-13)) {  // the exact reference sum
                 double exact = 0.0;
-                for (int s = 0; s < sp.S; ++s)
-                    if (c[s]) exact = __dadd_rn(exact, __ddiv_rn((double)c[s], a.tab.mean_service[rb + s]));
+                for (unsigned m = nz; m; m &= m - 1u) {  // parts order (ascending shape)
+                    const int s = __ffs(m) - 1;
+                    exact = __dadd_rn(exact, __ddiv_rn((double)c[s], a.tab.mean_service[rb + s]));
+                }
                 stable_plan = rd.rate < exact;
             }
             if (stable_plan) {
