@@ -1,6 +1,7 @@
 #!/bin/bash
 # One GPU session: parity tests, the benchmark line, ncu launch list and full
-# captures of the two graded kernels.  Usage: tools/gpu_job.sh [tests] [bench] [ncu]
+# captures of the two graded kernels.  Usage: tools/gpu_job.sh [tests] [bench] [ncu] [dev]
+#   dev: the K4 parity subset, a C2 timing and a per-launch table (the edit loop)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 what="${*:-tests bench ncu}"
@@ -8,6 +9,14 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gp
 if [[ $what == *tests* ]]; then
   timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
   tail -5 gpurun_out/pytest_gpu.log
+fi
+if [[ $what == *dev* ]]; then
+  timeout 900 python -m pytest tests -x -q -m gpu -k "k4 or golden or live_reference or medium or full_c2 or two_rank" \
+      > gpurun_out/dev_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/dev_pytest.log
+  timeout 300 python tools/perf_probe.py C2 - 1 3 2>&1 | tail -2
+  timeout 600 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active \
+      --clock-control none --csv --log-file gpurun_out/dev_launches.csv python tools/perf_probe.py C2 - 1 1 > /dev/null 2>&1
+  python tools/launch_table.py gpurun_out/dev_launches.csv | tail -1
 fi
 if [[ $what == *bench* ]]; then
   timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
