@@ -229,6 +229,8 @@ void* cg_engine_stream(cg_engine* engine);
  *   "sort_key"         3 (default) work-list order estimate (0 raw service bound)
  *   "class_order"      1 (default) replica-count classes ascending (0 descending)
  *   "wave_plans"       64 (default) plans per filter wave in units of 2^20 (~248 B of HBM per plan)
+ *   "conc_lists_max"   65536 (default) waves with at most this many listed plans run their
+ *                      replica-count classes concurrently on four streams (0: never)
  *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle" (diagnostic)
  * Unknown keys return CG_ERR_INVALID_INPUT. */
 cg_status cg_engine_set_option(cg_engine* engine, const char* key, int64_t value);

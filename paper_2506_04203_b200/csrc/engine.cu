@@ -146,6 +146,7 @@ struct cg_engine {
     int sm_count = 148;
     cudaStream_t s = nullptr;
     cudaStream_t s2 = nullptr;  // second stream: the concurrent pilot launch
+    cudaStream_t s3 = nullptr, s4 = nullptr;  // with s and s2: concurrent class lists of small waves
     int rank = 0, world = 1;
     cg_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
@@ -159,6 +160,7 @@ struct cg_engine {
     int pilot_sort = 1;             // pilot lists in ascending estimate order (option pilot_sort)
     int sort_key = 3;   // list/pilot order (option sort_key): 0 service bound, else an estimate (k_plan_filter)
     int class_order = 1;  // 0: lists by replica count descending, 1: ascending (option class_order)
+    long long conc_lists_max = 1 << 16;  // waves with at most this many listed plans run classes concurrently
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
@@ -174,7 +176,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_cperm, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -331,7 +333,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     CG_CUDA(cudaMemsetAsync(ovfcnt, 0, 8 * 8, x.s));
     unsigned long long* ovfcnt2 = E.d_ovfcnt2.as<unsigned long long>(1);
     unsigned long long* ctrs = E.d_ctrs.as<unsigned long long>(CTR_COUNT);
-    unsigned long long* ictr = E.d_ictr.as<unsigned long long>(2);  // [1]: the concurrent pilot launch
+    unsigned long long* ictr = E.d_ictr.as<unsigned long long>(4);  // one per concurrent launch region
     CG_CUDA(cudaMemsetAsync(tiecnt, 0, 8, x.s));
     CG_CUDA(cudaMemsetAsync(ctrs, 0, 8 * CTR_COUNT, x.s));
 
@@ -362,8 +364,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         max_slots = std::max(max_slots, sim_geometry(cls, SIM_DEEP, E.sm_count).slots);
     }
     const int sld = (n_req + 3) & ~3;  // 32-byte scratch columns
-    // two scratch regions: the pilot's two launches run concurrently
-    double* scratch = E.d_scratch.as<double>((size_t)2 * max_slots * sld);
+    // scratch regions for concurrent launches: the pilot's two, or up to four
+    // class lists of a small wave
+    const int nregions = E.conc_lists_max > 0 ? 4 : 2;
+    double* scratch = E.d_scratch.as<double>((size_t)nregions * max_slots * sld);
     int ring_cap = 1;
     while (ring_cap < n_req) ring_cap <<= 1;
 
@@ -612,20 +616,53 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                 CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
                 pilot_join = false;
             }
+            // Small waves are latency-bound (each launch lasts at least one
+            // plan's request chain): their class lists run concurrently, each on
+            // its own stream, scratch region, item counter and perm slice.
+            // Large waves run the classes in order so bounds tighten between them.
+            unsigned long long total = 0;
+            for (int c = 0; c < 7; ++c) total += counts[c];
+            const bool conc = total <= (unsigned long long)E.conc_lists_max;
+            unsigned long long* cperm = conc ? E.d_cperm.as<unsigned long long>(std::max<unsigned long long>(total, 1)) : nullptr;
+            unsigned long long poff = 0;
+            int nlaunched = 0;
+            cudaStream_t streams[4] = {x.s, E.s2, E.s3, E.s4};
+            if (conc) CG_CUDA(cudaEventRecord(E.ev[12], x.s));  // re-recorded after the sorts below
             for (int ci = 0; ci < 7; ++ci) {
                 const int c = E.class_order ? ci : 6 - ci;
                 unsigned long long* items = lists + (size_t)c * cap;
                 const unsigned long long* perm = nullptr;
-                if (E.prune && counts[c] > 1) {  // ascending service bound (16-bit key: 2 passes) of slot indices
+                if (E.prune && counts[c] > 1) {  // ascending order key (16 bits: 2 passes) of slot indices
                     k_iota_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(tidx, (long long)counts[c]);
                     CG_LAUNCH_CHECK();
                     ++x.launches;
                     const int par = radix_sort_u64(lkeys + (size_t)c * cap, tidx, tk, tv, (long long)counts[c],
                                                    (1ull << kListKeyBits) - 1ull, rsh, x.s, &x.launches);
                     perm = par ? tv : tidx;
+                    if (conc) {  // the shared sort buffers are reused by the next class
+                        CG_CUDA(cudaMemcpyAsync(cperm + poff, perm, counts[c] * 8, cudaMemcpyDeviceToDevice, x.s));
+                        perm = cperm + poff;
+                        poff += counts[c];
+                    }
                 }
-                run_list(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm);
+                if (!conc) {
+                    run_list(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm);
+                    continue;
+                }
+                if (counts[c] == 0) continue;
+                const int k = nlaunched++ % 4;
+                if (k > 0) {
+                    CG_CUDA(cudaEventRecord(E.ev[12], x.s));
+                    CG_CUDA(cudaStreamWaitEvent(streams[k], E.ev[12], 0));
+                }
+                run_list_on(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm,
+                            streams[k], k);
             }
+            if (conc)
+                for (int k = 1; k < 4 && k < nlaunched; ++k) {
+                    CG_CUDA(cudaEventRecord(E.ev[12 + k], streams[k]));
+                    CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[12 + k], 0));
+                }
         }
     }
     CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));  // the pilot's second stream (no-op if unused)
@@ -1425,6 +1462,8 @@ cg_status cg_engine_create(int32_t device, cg_engine** out) {
         e->sm_count = prop.multiProcessorCount;
         CG_CUDA(cudaStreamCreateWithFlags(&e->s, cudaStreamNonBlocking));
         CG_CUDA(cudaStreamCreateWithFlags(&e->s2, cudaStreamNonBlocking));
+        CG_CUDA(cudaStreamCreateWithFlags(&e->s3, cudaStreamNonBlocking));
+        CG_CUDA(cudaStreamCreateWithFlags(&e->s4, cudaStreamNonBlocking));
         for (auto& ev : e->ev) CG_CUDA(cudaEventCreate(&ev));
         *out = e;
     });
@@ -1438,6 +1477,8 @@ void cg_engine_destroy(cg_engine* e) {
     for (auto& ev : e->ev) cudaEventDestroy(ev);
     if (e->s) cudaStreamDestroy(e->s);
     if (e->s2) cudaStreamDestroy(e->s2);
+    if (e->s3) cudaStreamDestroy(e->s3);
+    if (e->s4) cudaStreamDestroy(e->s4);
     delete e;
 }
 
@@ -1467,6 +1508,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "class_order") e->class_order = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
         else if (k == "pilot_sort") e->pilot_sort = (int)value;
+        else if (k == "conc_lists_max") e->conc_lists_max = std::max<int64_t>(0, value);
         else if (k == "pilot_merge") e->pilot_merge = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "wave_plans") e->wave_plans = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
         else if (k == "item_plans") e->item_plans = (int)std::max<int64_t>(1, value);
