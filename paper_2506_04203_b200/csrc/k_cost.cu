@@ -869,6 +869,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
     unsigned long long plan = 0;
     bool ovf = false;
     unsigned lazy = 0;
+    unsigned mcur = 0;  // this step's idle mask (avail[r] <= t), computed one step ahead
     double U = INF;
     const double* Trow = a.tab.T;  // valid dummies until a plan is acquired
     const double* Orow = a.tab.O;
@@ -947,6 +948,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                             avail[r] = 0.0;
                         }
                     }
+                    mcur = 0;  // every replica starts idle (avail 0 <= T[0])
+#pragma unroll
+                    for (int r = 0; r < R; ++r) mcur |= (gl * R + r < dp) ? (1u << r) : 0u;
                     k = 0;
                     ab = 0;
                     ovf = false;
@@ -974,12 +978,15 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
         // ---- phase B: UNROLL request-steps per running plan, as pairs (rows
         // and k are even-aligned) with the next pair's arrivals/outputs
         // prefetched -- the lanes' rows differ, so they come from L2
-        auto step = [&](const double t, const double o) {
+        auto step = [&](const double t, const double o, const double tn1) {
             const bool run = status == ST_RUN;
-            unsigned m = 0;
+            const unsigned m = run ? mcur : 0u;
+            // next step's idle mask from the current avail (tn1 = next arrival),
+            // off the critical path; the winner's bit is fixed once its finish
+            // time is known
+            unsigned mn = 0;
 #pragma unroll
-            for (int r = 0; r < R; ++r) m |= (avail[r] <= t) ? (1u << r) : 0u;
-            m = run ? m : 0u;
+            for (int r = 0; r < R; ++r) mn |= (avail[r] <= tn1) ? (1u << r) : 0u;
             bool idle;
             int wlane;
             if (W == 1) {
@@ -1102,7 +1109,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     }
                 ab += soj > U ? 1 : 0;
                 scratch[k] = soj;
+                mn = (mn & ~(1u << rr)) | ((fin <= tn1) ? (1u << rr) : 0u);
             }
+            mcur = mn;
             k += run ? 1 : 0;
             status = (run && k == n_req) ? ST_FINISH : status;
         };
@@ -1112,6 +1121,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             const bool odd = (u & 1) != 0;
             const double t = odd ? tq.y : tq.x;
             const double o = odd ? oq.y : oq.x;
+            const double tn1 = odd ? tq2.x : tq.y;  // the next request's arrival
             if (odd) {
                 tq = tq2;
                 oq = oq2;
@@ -1119,7 +1129,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 tq2 = *reinterpret_cast<const double2*>(Trow + kp);
                 oq2 = *reinterpret_cast<const double2*>(Orow + kp);
             }
-            step(t, o);
+            step(t, o, tn1);
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
