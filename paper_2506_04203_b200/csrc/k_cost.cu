@@ -1004,7 +1004,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             const int pidx0 = (rr > 0 ? rr : 0) * 32 + lane;
             double fin = __dadd_rn(__dadd_rn(t, pre_s[pidx0]), __dmul_rn(o, dec_s[pidx0]));
             unsigned H = 0;
-            if (__any_sync(FULL, busy)) {
+            // W == 1: each lane is its own plan, plain divergent control flow
+            // (no warp vote on the step path)
+            if (W == 1 ? busy : __any_sync(FULL, busy)) {
                 if (busy && lazy) {
 #pragma unroll
                     for (int r = 0; r < R; ++r)
@@ -1021,7 +1023,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     dep[r] = busy && nd[r] <= t;
                     anydep |= dep[r];
                 }
-                while (__any_sync(FULL, anydep)) {
+                while (W == 1 ? anydep : __any_sync(FULL, anydep)) {
                     anydep = false;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
