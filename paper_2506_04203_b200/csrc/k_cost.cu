@@ -1103,12 +1103,12 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 }
                 lazy |= idle ? (1u << rr) : 0u;
 #pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (r == rr) {
-                        avail[r] = fin;
-                        ht[r] = H;
-                        if (HO && first) ho[r] = o;
-                    }
+                for (int r = 0; r < R; ++r) {  // straight-line selects (no per-replica branch)
+                    const bool hit = r == rr;
+                    avail[r] = hit ? fin : avail[r];
+                    ht[r] = hit ? H : ht[r];
+                    if (HO) ho[r] = (hit && first) ? o : ho[r];
+                }
                 ab += soj > U ? 1 : 0;
                 scratch[k] = soj;
                 mn = (mn & ~(1u << rr)) | ((fin <= tn1) ? (1u << rr) : 0u);
