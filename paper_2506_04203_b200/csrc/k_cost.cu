@@ -1092,28 +1092,28 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             }
             const bool me = run && gl == wlane;
             const double soj = __dsub_rn(fin, t);
-            if (me) {
-                // idle: the FIFO now holds just this job (lazy reset; H = 0 is
-                // an empty ring).  Busy: the job joins the queue.
-                const bool first = !idle && ((H >> 16) == (H & 0xffffu));  // the ring was empty
-                if (!idle) {
-                    ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
-                    H += 1u << 16;
-                    ovf |= (((H >> 16) - H) & 0xffffu) > (unsigned)CAP;
-                }
-                lazy |= idle ? (1u << rr) : 0u;
+            {
+                // predicated on `me` throughout (no branch).  Idle: the FIFO now
+                // holds just this job (lazy reset; H = 0 is an empty ring).
+                // Busy: the job joins the queue.
+                const bool push = me && !idle;
+                const bool first = push && ((H >> 16) == (H & 0xffffu));  // the ring was empty
+                if (push) ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
+                H += push ? (1u << 16) : 0u;
+                ovf |= push && ((((H >> 16) - H) & 0xffffu) > (unsigned)CAP);
+                lazy |= (me && idle) ? (1u << rr) : 0u;
 #pragma unroll
-                for (int r = 0; r < R; ++r) {  // straight-line selects (no per-replica branch)
-                    const bool hit = r == rr;
+                for (int r = 0; r < R; ++r) {
+                    const bool hit = me && r == rr;
                     avail[r] = hit ? fin : avail[r];
                     ht[r] = hit ? H : ht[r];
                     if (HO) ho[r] = (hit && first) ? o : ho[r];
                 }
-                ab += soj > U ? 1 : 0;
-                scratch[k] = soj;
-                mn = (mn & ~(1u << rr)) | ((fin <= tn1) ? (1u << rr) : 0u);
+                ab += (me && soj > U) ? 1 : 0;
+                if (me) scratch[k] = soj;
+                const unsigned rb = me ? (1u << rr) : 0u;
+                mcur = (mn & ~rb) | ((fin <= tn1) ? rb : 0u);
             }
-            mcur = mn;
             k += run ? 1 : 0;
             status = (run && k == n_req) ? ST_FINISH : status;
         };
