@@ -1027,7 +1027,22 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     anydep = false;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        if (dep[r]) {
+                        if (R <= 4) {  // few replicas: straight-line selects, predicated loads
+                            const unsigned h = ht[r] & 0xffffu;
+                            const unsigned tl = ht[r] >> 16;
+                            const bool pop = dep[r] && h != tl;
+                            double oh = 0.0;
+                            if (HO) oh = ho[r];
+                            else if (pop) oh = Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
+                            const double nx = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
+                                                        __dmul_rn(oh, dec_s[r * 32 + lane]));
+                            nd[r] = pop ? nx : (dep[r] ? INF : nd[r]);
+                            const unsigned h1 = (h + 1u) & 0xffffu;
+                            ht[r] = pop ? ((ht[r] & 0xffff0000u) | h1) : ht[r];
+                            if (HO && pop && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
+                            dep[r] = dep[r] && nd[r] <= t;
+                            anydep |= dep[r];
+                        } else if (dep[r]) {
                             const unsigned h = ht[r] & 0xffffu;
                             const unsigned tl = ht[r] >> 16;
                             if (h != tl) {  // the head job enters service
