@@ -1122,7 +1122,10 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     const bool hit = me && r == rr;
                     avail[r] = hit ? fin : avail[r];
                     ht[r] = hit ? H : ht[r];
-                    if (HO) ho[r] = (hit && first) ? o : ho[r];
+                }
+                if (HO && first) {  // the job is the head of an empty ring (rarer than a step)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
                 }
                 ab += (me && soj > U) ? 1 : 0;
                 if (me) scratch[k] = soj;
