@@ -1009,11 +1009,11 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             if (W == 1 ? busy : __any_sync(FULL, busy)) {
                 if (busy && lazy) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r)
-                        if ((lazy >> r) & 1u) {
-                            nd[r] = avail[r];
-                            ht[r] = (ht[r] & 0xffff0000u) | (ht[r] >> 16);
-                        }
+                    for (int r = 0; r < R; ++r) {  // selects, no per-replica branch
+                        const bool lz = (lazy >> r) & 1u;
+                        nd[r] = lz ? avail[r] : nd[r];
+                        ht[r] = lz ? ((ht[r] & 0xffff0000u) | (ht[r] >> 16)) : ht[r];
+                    }
                     lazy = 0;
                 }
                 bool dep[R];
@@ -1045,16 +1045,16 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                         } else if (dep[r]) {
                             const unsigned h = ht[r] & 0xffffu;
                             const unsigned tl = ht[r] >> 16;
-                            if (h != tl) {  // the head job enters service
-                                const double oh = HO ? ho[r] : Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
-                                nd[r] = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
-                                                  __dmul_rn(oh, dec_s[r * 32 + lane]));
-                                const unsigned h1 = (h + 1u) & 0xffffu;
-                                ht[r] = (ht[r] & 0xffff0000u) | h1;
-                                if (HO && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
-                            } else {
-                                nd[r] = INF;
-                            }
+                            const bool more = h != tl;  // the head job enters service
+                            double oh = 0.0;
+                            if (HO) oh = ho[r];
+                            else if (more) oh = Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
+                            const double nx = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
+                                                        __dmul_rn(oh, dec_s[r * 32 + lane]));
+                            nd[r] = more ? nx : INF;
+                            const unsigned h1 = (h + 1u) & 0xffffu;
+                            ht[r] = more ? ((ht[r] & 0xffff0000u) | h1) : ht[r];
+                            if (HO && more && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
                             dep[r] = nd[r] <= t;
                             anydep |= dep[r];
                         }
