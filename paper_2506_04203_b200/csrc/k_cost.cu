@@ -920,9 +920,11 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     gpus = gs.used;
                     plan = gs.plan;
                     const long long rb = (long long)row * kMaxShapes;
-                    const int S = a.spaces[a.rows[row].space].S;
                     Trow = a.tab.T + (long long)row * a.tab.ld;
                     Orow = a.tab.O + (long long)row * a.tab.ld;
+                    // replicas j = gl*R + r in parts order: one merged pass
+                    int q = 0, cum = 0, sh = -1;
+                    const int np = gs.nparts;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
@@ -930,21 +932,20 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                         ht[r] = 0;
                         avail[r] = INF;
                         if (j < dp) {
-                            int cum = 0, s = 0;
-                            if (gs.nparts > 0) {
-                                for (int q = 0; q < gs.nparts; ++q) {
-                                    s = gs.pshape[q];
+                            if (np > 0) {
+                                while (j >= cum) {
+                                    sh = gs.pshape[q];
                                     cum += gs.pcount[q];
-                                    if (j < cum) break;
+                                    ++q;
                                 }
                             } else {
-                                for (; s < S; ++s) {
-                                    cum += gs.counts[s];
-                                    if (j < cum) break;
+                                while (j >= cum) {
+                                    ++sh;
+                                    cum += gs.counts[sh];
                                 }
                             }
-                            pre_s[r * 32 + lane] = a.tab.prefill[rb + s];
-                            dec_s[r * 32 + lane] = a.tab.decode[rb + s];
+                            pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
+                            dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
                             avail[r] = 0.0;
                         }
                     }
