@@ -86,6 +86,19 @@ __global__ void k_iota_u64(unsigned long long* p, long long n) {
     if (i < n) p[i] = (unsigned long long)i;
 }
 
+// Work list in sorted order: out*[i] = in*[perm[i]] (so a plan claim is one dependent load, not two).
+__global__ void k_gather3_u64(const unsigned long long* __restrict__ perm, long long n,
+                              const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
+                              const unsigned long long* __restrict__ c, unsigned long long* __restrict__ oa,
+                              unsigned long long* __restrict__ ob, unsigned long long* __restrict__ oc) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long j = perm[i];
+    oa[i] = a[j];
+    ob[i] = b[j];
+    oc[i] = c[j];
+}
+
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -176,7 +189,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_cperm, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_cperm, d_gitems, d_gparts, d_gparts2, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -646,7 +659,23 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     }
                 }
                 if (!conc) {
-                    run_list(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm);
+                    const unsigned long long* li = items;
+                    const unsigned long long* lp = lparts + (size_t)c * cap;
+                    const unsigned long long* lp2 = lparts2 + (size_t)c * cap;
+                    if (perm) {  // gather into sorted order (the class lists run one after another)
+                        unsigned long long* gi = E.d_gitems.as<unsigned long long>(cap);
+                        unsigned long long* gp = E.d_gparts.as<unsigned long long>(cap);
+                        unsigned long long* gp2 = E.d_gparts2.as<unsigned long long>(cap);
+                        k_gather3_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(
+                            perm, (long long)counts[c], li, lp, lp2, gi, gp, gp2);
+                        CG_LAUNCH_CHECK();
+                        ++x.launches;
+                        li = gi;
+                        lp = gp;
+                        lp2 = gp2;
+                        perm = nullptr;
+                    }
+                    run_list(li, counts[c], c, false, lp, lp2, perm);
                     continue;
                 }
                 if (counts[c] == 0) continue;
