@@ -9,10 +9,19 @@ min-max solve, Tchebycheff + Pareto).  The metric's numerator is the number of
 reference's own count (sum over its row cache of |plan set|), identical for
 both arms -- and the denominator the sweep time.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+The default workload is C3 (BASELINE.json configs[2], the north-star config:
+3-model Llama 8B->70B->405B cascade, 1M-request bursty trace, 64-GPU pool).
 
 N>1 runs under torchrun: every rank routes redundantly, the cost-model work is
 sharded over ranks and merged with one NCCL all-gather (strong scaling).
+
+--impl reference times the reference CPU planner (oracle/_ref, compiled from
+the unmodified reference sources) on a bounded sample of the same workload and
+extrapolates the full sweep's time as a lower bound (oracle/cpu_baseline.py);
+its trace comes from the reference's own generator and it never loads the
+engine library.
 """
 from __future__ import annotations
 
@@ -49,11 +58,16 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def build_workload(name: str):
-    from paper_2506_04203_b200 import engine as eng
+def build_workload(name: str, generate=None):
+    """The config's synthetic trace and planner config.  `generate` defaults
+    to the engine's bit-identical generator; the reference arm passes the
+    reference's own cli::generate_trace (oracle/_ref) so it never loads the
+    engine library."""
     from paper_2506_04203_b200 import workloads as W
-    parts = [eng.generate_trace(s, seed) for s, seed in W.trace_specs(name)]
-    trace = eng.concat_traces(parts) if len(parts) > 1 else parts[0]
+    if generate is None:
+        from paper_2506_04203_b200 import engine as eng
+        generate = eng.generate_trace
+    trace = W.build_trace(name, generate)
     cfg, N = W.planner_config(name, trace["scores"])
     return trace, cfg, N
 
@@ -108,28 +122,20 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_reference_sample(trace, cfg, N, grid_points=4):
-    """The reference CPU planner (oracle/_ref, unmodified sources) timed on a
-    bounded sample of the same workload: same trace/hardware/models, a
-    grid_points^(C-1) threshold grid.  Returns (plans/s, details)."""
-    from oracle import refpy
-    from paper_2506_04203_b200 import workloads as W
-    sample_cfg = json.loads(json.dumps(cfg))
-    sample_cfg["sweep"]["threshold_grid"] = W.explicit_grid(trace["scores"], grid_points)
-    counts = refpy.plan_count(trace, sample_cfg, N)
-    t0 = time.perf_counter()
-    res = refpy.sweep(trace, sample_cfg, N)
-    wall = time.perf_counter() - t0
-    el = float(res["elapsed_s"])
-    cores = refpy.max_threads()
-    return counts["plans"] / el, {
-        "elapsed_s": el, "wall_s": wall, "plans": counts["plans"], "unique_rows": counts["unique_rows"],
-        "candidates": counts["candidates"], "cores": cores,
-        "sample": f"same trace/models/hardware, {grid_points}^(C-1) grid ({counts['candidates']} candidates, "
-                  f"{counts['unique_rows']} rows, {counts['plans']} plans), CASCADE_PLANNER_THREADS={cores}"}
+def config_keys(name, trace, N, ref: dict) -> dict:
+    """The `config` object both arms print (same keys, same values)."""
+    return {"workload": WORKLOAD_DESC.get(name, name), "total_gpus_planned": N,
+            "requests": int(trace["arrival_s"].shape[0]), "stages": int(trace["scores"].shape[0]),
+            "candidates": ref["candidates"], "unique_rows": ref["unique_rows"], "plans_per_sweep": ref["plans"],
+            "l2": "flushed (256 MiB write) before every timed step, outside the events"}
 
 
 def run_reference(args):
+    """The reference CPU planner (oracle/_ref: the unmodified reference
+    sources) on this config: every step times a bounded sample of reference
+    calls on all host threads and extrapolates the full sweep's time as a
+    lower bound (oracle/cpu_baseline.py); value = the sweep's plans / that
+    time.  Rank 0 only; the engine library is never loaded here."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -138,23 +144,33 @@ def run_reference(args):
     if not refpy.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcascade_ref.so not built"}))
         return 0
-    trace, cfg, N = build_workload(args.config)
+    from oracle import cpu_baseline
+    trace, cfg, N = build_workload(args.config, refpy.generate_trace)
+    ref = cpu_baseline.ReferenceSample(trace, cfg, N)
     for _ in range(args.warmup):
-        cpu_reference_sample(trace, cfg, N, args.ref_grid)
-    vals, dets = [], []
-    for _ in range(args.steps):
-        v, d = cpu_reference_sample(trace, cfg, N, args.ref_grid)
-        vals.append(v)
-        dets.append(d)
-    value = float(np.mean(vals))
-    ms = float(np.mean([d["elapsed_s"] for d in dets]) * 1000.0)
+        ref.step()
+    steps = [ref.step() for _ in range(args.steps)]
+    sweep_s = float(np.mean([s["sweep_s_lower_bound"] for s in steps]))
+    sample_s = float(np.mean([s["sample_s"] for s in steps]))
+    d = ref.describe()
+    value = d["plans"] / sweep_s
+    cfg_keys = config_keys(args.config, trace, N, {"candidates": d["candidates"], "unique_rows": d["unique_rows"],
+                                                   "plans": d["plans"]})
+    cfg_keys["parallelism"] = f"CPU threads: {d['threads']}"
+    kind = steps[-1]["kind"]
+    base = {"value": value, "unit": UNIT, "cores": d["threads"], "kind": "reference",
+            "sample": ref.sample_text(), "extrapolation": kind}
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "sample": dets[0]["sample"]},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": dets[0]["cores"], "kind": "reference",
-                            "sample": dets[0]["sample"]},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": sweep_s * 1000.0,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": cfg_keys,
+           "extrapolated": {"kind": kind, "sweep_s": sweep_s,
+                            "sweep_s_estimate": float(np.mean([s["sweep_s_estimate"] for s in steps])),
+                            "measured_sample_s_per_step": sample_s, "census": d,
+                            "last_step": steps[-1]},
+           "cpu_baseline": base,
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "kind": kind}}
     print(json.dumps(out), flush=True)
     return 0
 
@@ -317,11 +333,10 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_dev / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD_DESC.get(args.config, args.config), "total_gpus_planned": N,
-                       "requests": n, "stages": C, "candidates": st_dev[-1]["candidates"],
-                       "unique_rows": st_dev[-1]["unique_rows"], "plans_per_sweep": plans,
-                       "l2": "flushed (256 MiB write) before every timed step, outside the events",
-                       "parallelism": f"rows sharded over {world} GPU(s), 1 all-gather"},
+            "config": dict(config_keys(args.config, trace, N, {"candidates": st_dev[-1]["candidates"],
+                                                                "unique_rows": st_dev[-1]["unique_rows"],
+                                                                "plans": plans}),
+                           parallelism=f"rows sharded over {world} GPU(s), 1 all-gather"),
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
                     "h2d_bytes_per_step": st_e2e[-1]["h2d_bytes"], "d2h_bytes_per_step": st_e2e[-1]["d2h_bytes"]},
             "gpu_launches": int(sum(s["gpu_launches"] for s in st_dev) + sum(s["gpu_launches"] for s in st_e2e)),
@@ -342,9 +357,15 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             os.environ.setdefault("CASCADE_PLANNER_THREADS", str(os.cpu_count() or 1))
             try:
-                v, d = cpu_reference_sample(trace, cfg, N, args.ref_grid)
-                out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": d["cores"], "kind": "reference",
-                                       "sample": d["sample"], "elapsed_s": d["elapsed_s"]}
+                from oracle import cpu_baseline
+                ref = cpu_baseline.ReferenceSample(trace, cfg, N)
+                st = ref.step()
+                d = ref.describe()
+                out["cpu_baseline"] = {"value": d["plans"] / st["sweep_s_lower_bound"], "unit": UNIT,
+                                       "cores": d["threads"], "kind": "reference", "sample": ref.sample_text(),
+                                       "extrapolation": st["kind"], "sweep_s": st["sweep_s_lower_bound"],
+                                       "sweep_s_estimate": st["sweep_s_estimate"],
+                                       "measured_sample_s": st["sample_s"]}
             except Exception as ex:  # reported, never silently replaced
                 out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                                        "sample": f"unavailable: {ex}"}
@@ -361,8 +382,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOAD_DESC))
-    ap.add_argument("--ref-grid", type=int, default=4, help="grid points per dim of the CPU sample")
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOAD_DESC))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the 10M-request K1 roofline pass")
     args = ap.parse_args()

@@ -729,3 +729,183 @@ int co_sweep(const double* arrival, const double* in_tok, const double* out_tok,
     for (int d = 0; d < D; ++d) free(gv[d]);
     return OK;
 }
+
+/* ---------------- plan census (bench.py's CPU-baseline extrapolation only)
+ *
+ * For one row (model, workload, budget N): the number of plans the reference
+ * enumerates (enumerate_multisets, costmodel.cpp:132-146), and how many of
+ * them pass the stability test of StageEvaluator::row (costmodel.cpp:366-376:
+ * every part's shape memory-feasible at the p95 sequence length, and
+ * rate < sum over parts in shape order of cnt / mean_service[s]) -- i.e. how
+ * many queueing simulations the reference runs for that row -- binned by the
+ * replica count dp (bins: dp <= 4, 8, 16, 32, 64, 128, 256, > 256) together
+ * with the sum of dp per bin.  No simulation is run.  Threaded over prefixes
+ * of the enumeration (pthreads, dynamic task claiming). */
+#include <pthread.h>
+
+#define CENSUS_BINS 8
+
+typedef struct {
+    int S, N, L;
+    int size[MAXS];
+    char ok[MAXS];
+    double ms[MAXS];
+    double rate;
+    /* task prefixes: counts of shapes [0, L) */
+    int* prefix;
+    int64_t ntasks;
+    int64_t next;
+    pthread_mutex_t mu;
+    int64_t plans, stable, bin_n[CENSUS_BINS], bin_dp[CENSUS_BINS];
+} census_ctx;
+
+typedef struct {
+    int64_t plans, stable, bin_n[CENSUS_BINS], bin_dp[CENSUS_BINS];
+} census_acc;
+
+static int census_bin(int dp) {
+    int b = 0;
+    for (int lim = 4; b < CENSUS_BINS - 1 && dp > lim; lim *= 2) ++b;
+    return b;
+}
+
+/* level idx onward; cap = capacity of the parts so far (shape order), bad =
+ * some nonzero part is memory-infeasible */
+static void census_rec(const census_ctx* x, census_acc* a, int idx, int used, int dp, double cap, int bad) {
+    if (idx == x->S) {
+        if (used == 0) return;
+        a->plans++;
+        if (bad || x->rate >= cap) return;
+        a->stable++;
+        const int b = census_bin(dp);
+        a->bin_n[b]++;
+        a->bin_dp[b] += dp;
+        return;
+    }
+    const int size = x->size[idx];
+    for (int k = 0; used + k * size <= x->N; ++k) {
+        const double c2 = k > 0 ? cap + (double)k / x->ms[idx] : cap;
+        census_rec(x, a, idx + 1, used + k * size, dp + k, c2, bad || (k > 0 && !x->ok[idx]));
+    }
+}
+
+static int64_t census_prefixes(const census_ctx* x, int L, int* out) {
+    /* all count vectors of shapes [0, L) with sum of gpus <= N, recursion order */
+    int64_t n = 0;
+    int c[MAXS];
+    memset(c, 0, sizeof(c));
+    int used = 0, lvl = 0;
+    /* iterative odometer over levels [0, L) */
+    for (;;) {
+        if (lvl == L) {
+            if (out) memcpy(out + n * L, c, sizeof(int) * L);
+            ++n;
+            /* advance */
+            --lvl;
+            while (lvl >= 0) {
+                if (used + x->size[lvl] <= x->N) {
+                    c[lvl]++;
+                    used += x->size[lvl];
+                    ++lvl;
+                    break;
+                }
+                used -= c[lvl] * x->size[lvl];
+                c[lvl] = 0;
+                --lvl;
+            }
+            if (lvl < 0) break;
+            continue;
+        }
+        ++lvl;
+    }
+    return n;
+}
+
+static void* census_worker(void* arg) {
+    census_ctx* x = (census_ctx*)arg;
+    census_acc a;
+    memset(&a, 0, sizeof(a));
+    for (;;) {
+        pthread_mutex_lock(&x->mu);
+        const int64_t t = x->next++;
+        pthread_mutex_unlock(&x->mu);
+        if (t >= x->ntasks) break;
+        const int* c = x->prefix + t * x->L;
+        int used = 0, dp = 0, bad = 0;
+        double cap = 0.0;
+        for (int s = 0; s < x->L; ++s) {
+            used += c[s] * x->size[s];
+            dp += c[s];
+            if (c[s] > 0) {
+                cap = cap + (double)c[s] / x->ms[s];
+                bad = bad || !x->ok[s];
+            }
+        }
+        census_rec(x, &a, x->L, used, dp, cap, bad);
+    }
+    pthread_mutex_lock(&x->mu);
+    x->plans += a.plans;
+    x->stable += a.stable;
+    for (int b = 0; b < CENSUS_BINS; ++b) {
+        x->bin_n[b] += a.bin_n[b];
+        x->bin_dp[b] += a.bin_dp[b];
+    }
+    pthread_mutex_unlock(&x->mu);
+    return NULL;
+}
+
+/* out[0] = plans, out[1] = stable plans, out[2 + b] = stable plans in dp bin b,
+ * out[2 + CENSUS_BINS + b] = sum of dp over them. */
+int co_row_census(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
+                  int threads, int64_t* out) {
+    memset(out, 0, sizeof(int64_t) * (2 + 2 * CENSUS_BINS));
+    if (workload_invalid(w)) return E_INVALID;
+    census_ctx x;
+    memset(&x, 0, sizeof(x));
+    int tp[MAXS], pp[MAXS];
+    x.S = legal_shapes(m, hw, p, tp, pp);
+    if (max_budget < 1 || x.S == 0) return OK;
+    x.N = max_budget;
+    x.rate = w[0];
+    const double kv_tokens = w[3] + w[4];
+    const double clamped = w[2] * 0.98168436111126578;
+    for (int s = 0; s < x.S; ++s) {
+        x.size[s] = tp[s] * pp[s];
+        if (!mem_feasible(tp[s], pp[s], m, hw, p, kv_tokens)) continue;
+        x.ok[s] = 1;
+        const double gpus = tp[s] * pp[s];
+        const double bubble = 1.0 + p->bubble * (pp[s] - 1);
+        const double prefill = (2.0 * m->param_count * w[1] / (gpus * hw->flops * p->prefill_eff) + pp[s] * p->comm) * bubble;
+        const double decode = m->param_count * m->bytes_per_param / (tp[s] * hw->mem_bw * p->decode_eff) + pp[s] * p->comm;
+        x.ms[s] = prefill + clamped * decode;
+    }
+    if (w[0] == 0.0) { /* the reference returns an all-zero row without enumerating */
+        return OK;
+    }
+    if (threads < 1) threads = 1;
+    /* prefix depth: enough tasks to balance the threads */
+    int L = 0;
+    int64_t nt = 1;
+    while (L < x.S && nt < 256 * (int64_t)threads) {
+        ++L;
+        nt = census_prefixes(&x, L, NULL);
+    }
+    x.L = L;
+    x.ntasks = nt;
+    x.prefix = (int*)malloc(sizeof(int) * (size_t)(nt * (L > 0 ? L : 1)));
+    census_prefixes(&x, L, x.prefix);
+    pthread_mutex_init(&x.mu, NULL);
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+    for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, census_worker, &x);
+    for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+    pthread_mutex_destroy(&x.mu);
+    free(th);
+    free(x.prefix);
+    out[0] = x.plans;
+    out[1] = x.stable;
+    for (int b = 0; b < CENSUS_BINS; ++b) {
+        out[2 + b] = x.bin_n[b];
+        out[2 + CENSUS_BINS + b] = x.bin_dp[b];
+    }
+    return OK;
+}

@@ -58,4 +58,11 @@ int co_sweep(const double* arrival, const double* in_tok, const double* out_tok,
              int* eval_plan_counts, double* weights, int* sel, int64_t* front, int64_t* skipped,
              int64_t* counts, double* z);
 
+/* Plan census of one row for the CPU-baseline extrapolation (no simulation):
+ * out[0] = plans enumerated, out[1] = stable plans (= queueing simulations the
+ * reference runs), out[2+b] / out[10+b] = stable plans / sum of dp in replica
+ * bins b (dp <= 4, 8, 16, 32, 64, 128, 256, > 256).  threads = pthreads used. */
+int co_row_census(const co_model* m, const double* w, const co_hw* hw, const co_params* p, int max_budget,
+                  int threads, int64_t* out);
+
 #endif

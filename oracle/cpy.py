@@ -263,3 +263,25 @@ def sweep(trace, config, total_gpus):
             "weights": [{"lambda1": float(weights[2 * k]), "lambda2": float(weights[2 * k + 1])} for k in range(Wn)],
             "weight_selection": sel[:Wn].tolist(), "utopia": {"z1_star": float(z[0]), "z2_star": float(z[1])},
             "skipped": [{"thresholds": thresholds_of(skipped[s])} for s in range(S)]}
+
+
+CENSUS_BIN_LIMITS = [4, 8, 16, 32, 64, 128, 256, None]
+
+
+def row_census(hw, params, model, workload, max_budget, threads=None):
+    """Plans the reference enumerates for one row and how many pass its
+    stability test (= the queueing simulations StageEvaluator::row runs,
+    costmodel.cpp:366-376), binned by replica count.  No simulation."""
+    w = np.array([workload[k] for k in ("arrival_rate", "mean_input_tokens", "mean_output_tokens",
+                                        "p95_input_tokens", "p95_output_tokens")], dtype=np.float64)
+    out = np.zeros(18, dtype=np.int64)
+    hwc, mc, pc = _hw(hw), _model(model), _params(params)
+    L = lib()
+    L.co_row_census.restype = ctypes.c_int
+    rc = L.co_row_census(ctypes.byref(mc), _P(w), ctypes.byref(hwc), ctypes.byref(pc), int(max_budget),
+                         int(threads or os.cpu_count() or 1), _P(out))
+    if rc != -1:
+        raise OracleError(rc)
+    bins = [{"dp_max": lim, "stable": int(out[2 + b]), "sum_dp": int(out[10 + b])}
+            for b, lim in enumerate(CENSUS_BIN_LIMITS)]
+    return {"plans": int(out[0]), "stable": int(out[1]), "bins": bins}

@@ -23,7 +23,9 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <atomic>
 #include <map>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -482,6 +484,81 @@ char* ref_plan_count(const double* arrival, const double* in_tok, const double* 
         j["plans"] = plans;
         j["candidates"] = candidates;
         return ok(j, 0.0);
+    } catch (const CascadeError& e) {
+        return fail(e);
+    } catch (const std::exception& e) {
+        return fail_std(e);
+    }
+}
+
+/// The unique (stage, WorkloadStats) rows of a sweep -- the reference's own
+/// row-cache keys (outerplan.cpp:155-162, 191-203) -- from route_trace over
+/// every grid candidate (outerplan.cpp:221-239), the candidates routed
+/// concurrently on `threads` std::threads (route_trace is a pure function).
+/// Used only to size the CPU-baseline extrapolation in bench.py.  Reports
+/// the summed per-call route_trace time (what the sequential sweep spends).
+char* ref_unique_rows(const double* arrival, const double* in_tok, const double* out_tok,
+                      const double* scores, std::int64_t n, int c, const char* config_json,
+                      int total_gpus, int threads) {
+    try {
+        auto cfg = json::parse(config_json).get<cli::PlannerConfig>();
+        auto trace = make_trace(arrival, in_tok, out_tok, scores, n, c);
+        auto grid = cfg.sweep.threshold_grid.empty()
+                        ? outerplan::default_threshold_grid(trace, static_cast<std::size_t>(c))
+                        : cfg.sweep.threshold_grid;
+        std::vector<std::vector<double>> cands;
+        std::vector<std::size_t> cursor(grid.size(), 0);
+        for (bool done = false; !done;) {
+            std::vector<double> h;
+            for (std::size_t d = 0; d < grid.size(); ++d) h.push_back(grid[d][cursor[d]]);
+            cands.push_back(std::move(h));
+            done = true;
+            for (std::size_t d = grid.size(); d-- > 0;) {
+                if (++cursor[d] < grid[d].size()) { done = false; break; }
+                cursor[d] = 0;
+            }
+            if (grid.empty()) break;
+        }
+        std::vector<bool> deployed(c, true);
+        std::vector<routing::RoutingOutcome> outs(cands.size());
+        std::vector<double> secs(cands.size(), 0.0);
+        if (threads < 1) threads = 1;
+        std::vector<std::thread> pool;
+        std::atomic<std::size_t> next{0};
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                for (std::size_t i; (i = next.fetch_add(1)) < cands.size();) {
+                    RoutingThresholds h;
+                    h.thresholds = cands[i];
+                    auto t0 = std::chrono::steady_clock::now();
+                    outs[i] = routing::route_trace(trace, h, deployed);
+                    secs[i] = seconds_since(t0);
+                }
+            });
+        for (auto& t : pool) t.join();
+        std::map<std::string, std::pair<int, WorkloadStats>> rows;
+        double route_s = 0.0;
+        for (std::size_t k = 0; k < cands.size(); ++k) {
+            route_s += secs[k];
+            for (int i = 0; i < c; ++i) {
+                if (!(outs[k].ratios[i] > 0.0)) continue;
+                const auto& w = outs[k].stage_workloads[i];
+                double f[5] = {w.arrival_rate, w.mean_input_tokens, w.mean_output_tokens,
+                               w.p95_input_tokens, w.p95_output_tokens};
+                std::string key(sizeof(int) + sizeof(f), '\0');
+                std::memcpy(key.data(), &i, sizeof(int));
+                std::memcpy(key.data() + sizeof(int), f, sizeof(f));
+                rows.emplace(key, std::make_pair(i, w));
+            }
+        }
+        json list = json::array();
+        for (const auto& kv : rows) list.push_back({{"stage", kv.second.first}, {"workload", kv.second.second}});
+        json j;
+        j["rows"] = std::move(list);
+        j["candidates"] = cands.size();
+        j["route_calls_s"] = route_s;
+        j["total_gpus"] = total_gpus;
+        return ok(j, route_s);
     } catch (const CascadeError& e) {
         return fail(e);
     } catch (const std::exception& e) {

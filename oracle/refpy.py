@@ -47,6 +47,8 @@ def lib():
             "ref_pareto": [_D, _D, ctypes.c_int64],
             "ref_plan_count": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int],
             "ref_dump_sweep": [ctypes.c_char_p],
+            "ref_unique_rows": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int,
+                                ctypes.c_int],
             "ref_drift": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
                           ctypes.c_char_p, ctypes.c_int, ctypes.c_double],
             "ref_simulate": [_D, _D, _D, _D, ctypes.c_int64, ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p,
@@ -135,6 +137,14 @@ def plan_count(trace: dict, config: dict, total_gpus: int) -> dict:
     keep, n, c = _trace_args(trace)
     return _unwrap(_call(lib().ref_plan_count, *map(_ptr, keep), n, c, json.dumps(config).encode(),
                          total_gpus))["result"]
+
+
+def unique_rows(trace: dict, config: dict, total_gpus: int, threads: int = 0) -> dict:
+    """The sweep's unique (stage, WorkloadStats) rows, by the reference's own
+    route_trace over every candidate (routed on `threads` threads)."""
+    keep, n, c = _trace_args(trace)
+    return _unwrap(_call(lib().ref_unique_rows, *map(_ptr, keep), n, c, json.dumps(config).encode(),
+                         int(total_gpus), int(threads or os.cpu_count() or 1)))["result"]
 
 
 def route(trace: dict, thresholds, deployed) -> dict:

@@ -261,7 +261,9 @@ int row_class(const HostPlanSpace& sp, int N) {
     if (sp.min_gpus <= 0 || N < 1) return 3;
     const int dpmax = N / sp.min_gpus;
     const int cls = class_for_dp(dpmax);
-    if (cls < 0) fail(CG_ERR_UNSUPPORTED, "plans with more than 256 replicas are not supported");
+    if (cls < 0) fail(CG_ERR_UNSUPPORTED, "plans with more than 255 replicas are not supported");
+    if (sp.num_plans > kItemPlanMask)  // work items pack (row << 44) | plan
+        fail(CG_ERR_UNSUPPORTED, "plan space too large for 44-bit plan indices");
     return cls;
 }
 
@@ -272,6 +274,16 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     cg_engine& E = x.E;
     set_k4_pack(E.k4_pack == 3 && q.queueing_sim_requests > 65535 ? 1 : E.k4_pack);  // k_lane rings hold u16 request indices
     const int nrows = (int)rows.size();
+    if (rows.size() >= (1ull << (64 - kItemPlanBits)))
+        fail(CG_ERR_UNSUPPORTED, "too many unique rows for the 20-bit row field of a work item");
+    {
+        std::vector<char> seen(hs.size(), 0);  // replica-count and plan-index limits of every live space
+        for (const auto& rd : rows)
+            if (!seen[rd.space]) {
+                seen[rd.space] = 1;
+                row_class(hs[rd.space], N);
+            }
+    }
     const long long cells = (long long)nrows * (N + 1);
     const int n_req = q.queueing_sim_requests;
     if (nrows == 0) return;
@@ -284,10 +296,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     tab.mean_service = E.d_ms.as<double>((size_t)nrows * kMaxShapes);
     tab.inv_service = E.d_ims.as<double>((size_t)nrows * kMaxShapes);
     tab.ld = (n_req + 3) & ~3;
+    const std::vector<double> L = crn_log1p_table(q.queueing_sim_seed, n_req);  // glibc log1p (H3), once
     {
         // future-service bound tables (RowTables): requests ranked by output,
         // largest first (outputs are monotone in -L[2k+1], ties by index)
-        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
         std::vector<int> desc(n_req), pos(n_req);
         for (int k = 0; k < n_req; ++k) desc[k] = k;
         std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
@@ -295,10 +307,24 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         const int nc = (n_req + 31) / 32;
         std::vector<int> probe(nc);
         for (int i = 0; i < nc; ++i) probe[i] = desc[std::min(32 * i + 31, n_req - 1)];
-        std::vector<unsigned> fut((size_t)(nc + 1) * nc, 0u);
-        for (int c = 0; c <= nc; ++c)
-            for (int j = 32 * c; j < n_req; ++j)
-                for (int i = pos[j] / 32; i < nc; ++i) ++fut[(size_t)c * nc + i];
+        // fut[c][i] = #requests j >= 32c whose output rank block pos[j]/32 <= i,
+        // built backwards: fut[c] = fut[c+1] + the prefix histogram of block c
+        std::vector<unsigned> fut;
+        if (E.fut_bound) {
+            fut.assign((size_t)(nc + 1) * nc, 0u);
+            std::vector<unsigned> h(nc);
+            for (int c = nc - 1; c >= 0; --c) {
+                std::fill(h.begin(), h.end(), 0u);
+                for (int j = 32 * c; j < std::min(32 * c + 32, n_req); ++j) ++h[pos[j] / 32];
+                unsigned run = 0;
+                for (int i = 0; i < nc; ++i) {
+                    run += h[i];
+                    fut[(size_t)c * nc + i] = fut[(size_t)(c + 1) * nc + i] + run;
+                }
+            }
+        } else {
+            fut.assign(1, 0u);
+        }
         int* dprobe = E.d_probe.as<int>((size_t)nc);
         unsigned* dfut = E.d_fut.as<unsigned>(fut.size());
         x.h2d(dprobe, probe.data(), probe.size() * sizeof(int));
@@ -313,7 +339,6 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     CG_CUDA(cudaMemsetAsync(tab.T, 0, (size_t)nrows * tab.ld * 8, x.s));
     CG_CUDA(cudaMemsetAsync(tab.O, 0, (size_t)nrows * tab.ld * 8, x.s));
     {
-        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
         double* dL = E.d_crn.as<double>(L.size());
         x.h2d(dL, L.data(), L.size() * sizeof(double));
         RowSetupArgs ra;
@@ -354,7 +379,6 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     // index of the K-th largest CRN output: outputs are monotone in -L[2k+1]
     int kstar = 0;
     {
-        auto L = crn_log1p_table(q.queueing_sim_seed, n_req);
         std::vector<int> idx(n_req);
         for (int k = 0; k < n_req; ++k) idx[k] = k;
         std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });

@@ -1571,7 +1571,7 @@ int class_for_dp(int dpmax) {
     if (dpmax <= 32) return 3;
     if (dpmax <= 64) return 4;
     if (dpmax <= 128) return 5;
-    if (dpmax <= 256) return 6;
+    if (dpmax <= 255) return 6;  // replica counts are 8-bit (filter, packed parts, unrank)
     return -1;
 }
 

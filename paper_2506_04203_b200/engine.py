@@ -821,18 +821,8 @@ def merge_row_shards(hw: dict, params: Optional[dict], model: dict, max_budget: 
 
 def concat_traces(parts: Sequence[dict]) -> dict:
     """Concatenates trace segments with time offsets (bursty traces, C3)."""
-    arrs, ins, outs, scs = [], [], [], []
-    offset = 0.0
-    for p in parts:
-        a = np.asarray(p["arrival_s"]) + offset
-        if a.size:
-            offset = float(a[-1])
-        arrs.append(a)
-        ins.append(p["input_tokens"])
-        outs.append(p["output_tokens"])
-        scs.append(p["scores"])
-    return {"arrival_s": np.concatenate(arrs), "input_tokens": np.concatenate(ins),
-            "output_tokens": np.concatenate(outs, axis=1), "scores": np.concatenate(scs, axis=1)}
+    from . import workloads
+    return workloads.concat_traces(parts)
 
 
 _default_engine: Optional[Engine] = None
