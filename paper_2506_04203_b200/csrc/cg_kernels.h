@@ -117,15 +117,30 @@ constexpr int kListKeyBits = 16;
 constexpr int kItemPlanBits = 44;
 constexpr unsigned long long kItemPlanMask = (1ull << kItemPlanBits) - 1ull;
 
+// A filtered work item: the plan and everything a JSQ kernel needs to start
+// it without unranking or table walks (k_plan_filter writes, k_lane/k_sim read).
+//   w[0..2]: a 192-bit little-endian bit stream -- bits 0-3 the number of
+//            parts np (0: more than kRecMaxParts parts, unrank instead), bits
+//            4-12 the GPUs used, then np fields of 13 bits (5-bit shape index
+//            | 8-bit replica count << 5) in ascending shape order;
+//   lb:      the exact service-time lower bound of the plan's K-th largest
+//            sojourn (k_plan_filter's header comment), already with its
+//            1e-12 margins: sojourns below it never reach the p95.
+constexpr int kRecMaxParts = 13;
+struct ItemRec {
+    unsigned long long item;   // (row << 44) | plan index
+    unsigned long long w[3];
+    double lb;
+};
+
 struct SimArgs {
     int N, n_req, K, prune;
     int kstar;                                 // index of the K-th largest CRN output
     int check_stable;                          // 1: items are not pre-filtered (seeds)
     int seeds;                                 // 1: count completions as seeding work
-    const unsigned long long* items;           // packed (row, plan) work items
-    const unsigned long long* parts;           // optional: the items' shape multisets (see encode_parts)
-    const unsigned long long* parts2;          // optional: parts 4..7 and the part count (lane kernels)
-    const unsigned long long* perm;            // optional: item i is items[perm[i]] (sorted lists)
+    const unsigned long long* items;           // packed (row, plan) work items (when recs == nullptr)
+    const ItemRec* recs;                       // filtered items with parts and bound (else nullptr)
+    const unsigned long long* perm;            // optional: item i is items/recs[perm[i]] (sorted lists)
     unsigned long long nitems;
     unsigned long long* item_counter;
     const RowDesc* rows;
@@ -144,7 +159,23 @@ struct SimArgs {
     double* ring_global;                       // DEEP: [warps][32*R*ring_cap]
     int ring_cap;
     unsigned long long* counters;
+    // future-service bound snapshot: qtab[(row*(N+1) + g)*32 + s] = number of
+    // leading output-ranked request blocks whose every request's service on
+    // shape s exceeds ub[row][g] as it was when the table was built
+    // (k_fut_snapshot); a plan's count is the minimum over its shapes
+    const unsigned short* qtab;
 };
+
+// Future-bound snapshot (see SimArgs::qtab).
+struct FutSnapArgs {
+    int nrows, N, n_req;
+    const RowDesc* rows;
+    const PlanSpace* spaces;
+    RowTables tab;
+    const unsigned long long* ub;
+    unsigned short* qtab;
+};
+void launch_fut_snapshot(const FutSnapArgs& a, cudaStream_t s, int* launches);
 
 struct FilterArgs {
     int N, n_req, kstar, prune;
@@ -158,9 +189,7 @@ struct FilterArgs {
     const PlanSpace* spaces;
     RowTables tab;
     const unsigned long long* ub;
-    unsigned long long* lists[7];
-    unsigned long long* parts[7];              // shape multisets of the listed plans
-    unsigned long long* parts2[7];             // their parts 4..7 (encode_parts)
+    ItemRec* recs[7];                          // listed plans (ItemRec)
     unsigned long long* keys[7];               // coarse service-bound order keys
     unsigned long long* list_count;            // [7]
     unsigned long long list_cap;               // per class

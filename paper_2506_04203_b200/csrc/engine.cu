@@ -86,18 +86,14 @@ __global__ void k_iota_u64(unsigned long long* p, long long n) {
     if (i < n) p[i] = (unsigned long long)i;
 }
 
-// Work list in sorted order: out*[i] = in*[perm[i]] (so a plan claim is one dependent load, not two).
-__global__ void k_gather3_u64(const unsigned long long* __restrict__ perm, long long n,
-                              const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
-                              const unsigned long long* __restrict__ c, unsigned long long* __restrict__ oa,
-                              unsigned long long* __restrict__ ob, unsigned long long* __restrict__ oc) {
+// Work list in sorted order: out[i] = in[perm[i]] (so a plan claim is one dependent load, not two).
+__global__ void k_gather_recs(const unsigned long long* __restrict__ perm, long long n,
+                              const ItemRec* __restrict__ in, ItemRec* __restrict__ out) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const unsigned long long j = perm[i];
-    oa[i] = a[j];
-    ob[i] = b[j];
-    oc[i] = c[j];
+    out[i] = in[perm[i]];
 }
+
 
 __global__ void k_fill_u64(unsigned long long* p, long long n, unsigned long long v) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -189,7 +185,7 @@ struct cg_engine {
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
-        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lparts, d_lparts2, d_pilot, d_plists, d_pkeys, d_pperm, d_cperm, d_gitems, d_gparts, d_gparts2, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
+        d_eL, d_eQ, d_skip, d_weights, d_sel, d_pk0, d_pk1, d_pv0, d_pv1, d_pkl, d_front, d_fsize, d_misc, d_dep, d_accept, d_acc, d_part32, d_hiacc, d_lrecs, d_grecs, d_qtab, d_pilot, d_plists, d_pkeys, d_pperm, d_cperm, d_ptk, d_ptv, d_prsh, d_pcount, d_lidx, d_probe, d_fut, d_pv;
     IngestBuffers ingest;
     JsonBuffers jsonbuf;
     SimRunBuffers simbuf;
@@ -433,17 +429,32 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
 
     // Runs one packed work list through the class kernel; ring overflows are
     // appended to the class's overflow region.
-    auto run_list_on = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
-                           const unsigned long long* parts, const unsigned long long* parts2,
-                           const unsigned long long* perm, cudaStream_t st, int region) {
+    // future-bound snapshot of the live bounds, refreshed before every list launch
+    unsigned short* qtab = E.d_qtab.as<unsigned short>((size_t)cells * kMaxShapes);
+    base.qtab = (E.prune && tab.nc > 0) ? qtab : nullptr;
+    auto snapshot = [&](cudaStream_t st) {
+        if (!base.qtab) return;
+        FutSnapArgs fs{};
+        fs.nrows = nrows;
+        fs.N = N;
+        fs.n_req = n_req;
+        fs.rows = base.rows;
+        fs.spaces = base.spaces;
+        fs.tab = tab;
+        fs.ub = ub;
+        fs.qtab = qtab;
+        launch_fut_snapshot(fs, st, &x.launches);
+    };
+    auto run_list_on = [&](const unsigned long long* items, const ItemRec* recs, unsigned long long nitems,
+                           int cls, bool seeds, const unsigned long long* perm, cudaStream_t st, int region) {
         if (nitems == 0) return;
         CG_CUDA(cudaMemsetAsync(ictr + region, 0, 8, st));
+        snapshot(st);
         SimArgs a = base;
         a.item_counter = ictr + region;
         a.scratch = scratch + (size_t)region * max_slots * sld;
         a.items = items;
-        a.parts = parts;
-        a.parts2 = parts2;
+        a.recs = recs;
         a.perm = perm;
         a.nitems = nitems;
         a.check_stable = seeds ? 1 : 0;
@@ -453,10 +464,9 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         a.ovf_count = ovfcnt + slot;
         launch_sim(a, cls, SIM_LIST, E.sm_count, st, &x.launches, nullptr);
     };
-    auto run_list = [&](const unsigned long long* items, unsigned long long nitems, int cls, bool seeds,
-                        const unsigned long long* parts, const unsigned long long* parts2,
-                        const unsigned long long* perm) {
-        run_list_on(items, nitems, cls, seeds, parts, parts2, perm, x.s, 0);
+    auto run_list = [&](const unsigned long long* items, const ItemRec* recs, unsigned long long nitems, int cls,
+                        bool seeds, const unsigned long long* perm) {
+        run_list_on(items, recs, nitems, cls, seeds, perm, x.s, 0);
     };
     // Deep-queue re-runs (rings in global memory, capacity >= n_req) of every
     // overflowed plan, one launch per class.
@@ -474,8 +484,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
             SimArgs d = base;
             d.items = ovf + (size_t)cls * ovf_region;
-            d.parts = nullptr;
-            d.parts2 = nullptr;
+            d.recs = nullptr;
             d.perm = nullptr;
             d.nitems = novf[cls];
             d.ring_global = ring;
@@ -507,7 +516,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         if (!seeds.empty() && !use_pilot) {
             unsigned long long* dseeds = E.d_seeds.as<unsigned long long>(seeds.size());
             x.h2d(dseeds, seeds.data(), seeds.size() * 8);
-            run_list(dseeds, seeds.size(), 3, true, nullptr, nullptr, nullptr);
+            run_list(dseeds, nullptr, seeds.size(), 3, true, nullptr);
         }
     }
     // Filter waves: enumerate every plan once, keep stable + not-bounded plans
@@ -524,9 +533,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             std::max<unsigned long long>(1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk,
                                                                          c_hi - c_lo));
         const unsigned long long cap = wave_chunks * chunk;
-        unsigned long long* lists = E.d_lists.as<unsigned long long>((size_t)7 * cap);
-        unsigned long long* lparts = E.d_lparts.as<unsigned long long>((size_t)7 * cap);
-        unsigned long long* lparts2 = E.d_lparts2.as<unsigned long long>((size_t)7 * cap);
+        ItemRec* lrecs = E.d_lrecs.as<ItemRec>((size_t)7 * cap);
         unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cap);
         unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)7 * cap);
         unsigned long long* tk = E.d_lk1.as<unsigned long long>(cap);
@@ -611,9 +618,9 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             // class 0 (dp <= 4) on the second stream, concurrently with the rest
             CG_CUDA(cudaEventRecord(E.ev[10], x.s));
             CG_CUDA(cudaStreamWaitEvent(E.s2, E.ev[10], 0));
-            run_list_on(plists, pcounts[0], 0, true, nullptr, nullptr, pperm[0], E.s2, 1);
+            run_list_on(plists, nullptr, pcounts[0], 0, true, pperm[0], E.s2, 1);
             for (int c = 6; c >= 1; --c)
-                run_list(plists + (size_t)c * pregion, pcounts[c], c, true, nullptr, nullptr, pperm[c]);
+                run_list(plists + (size_t)c * pregion, nullptr, pcounts[c], c, true, pperm[c]);
             CG_CUDA(cudaEventRecord(E.ev[11], E.s2));
             pilot_join = true;  // joined before the first bulk list: it overlaps the wave filter
         }
@@ -636,9 +643,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fa.tab = tab;
             fa.ub = ub;
             for (int c = 0; c < 7; ++c) {
-                fa.lists[c] = lists + (size_t)c * cap;
-                fa.parts[c] = lparts + (size_t)c * cap;
-                fa.parts2[c] = lparts2 + (size_t)c * cap;
+                fa.recs[c] = lrecs + (size_t)c * cap;
                 fa.keys[c] = lkeys + (size_t)c * cap;
             }
             fa.list_count = lcount;
@@ -667,7 +672,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             if (conc) CG_CUDA(cudaEventRecord(E.ev[12], x.s));  // re-recorded after the sorts below
             for (int ci = 0; ci < 7; ++ci) {
                 const int c = E.class_order ? ci : 6 - ci;
-                unsigned long long* items = lists + (size_t)c * cap;
+                const ItemRec* recs = lrecs + (size_t)c * cap;
                 const unsigned long long* perm = nullptr;
                 if (E.prune && counts[c] > 1) {  // ascending order key (16 bits: 2 passes) of slot indices
                     k_iota_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(tidx, (long long)counts[c]);
@@ -683,23 +688,17 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     }
                 }
                 if (!conc) {
-                    const unsigned long long* li = items;
-                    const unsigned long long* lp = lparts + (size_t)c * cap;
-                    const unsigned long long* lp2 = lparts2 + (size_t)c * cap;
+                    const ItemRec* lr = recs;
                     if (perm) {  // gather into sorted order (the class lists run one after another)
-                        unsigned long long* gi = E.d_gitems.as<unsigned long long>(cap);
-                        unsigned long long* gp = E.d_gparts.as<unsigned long long>(cap);
-                        unsigned long long* gp2 = E.d_gparts2.as<unsigned long long>(cap);
-                        k_gather3_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(
-                            perm, (long long)counts[c], li, lp, lp2, gi, gp, gp2);
+                        ItemRec* gr = E.d_grecs.as<ItemRec>(cap);
+                        k_gather_recs<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(
+                            perm, (long long)counts[c], lr, gr);
                         CG_LAUNCH_CHECK();
                         ++x.launches;
-                        li = gi;
-                        lp = gp;
-                        lp2 = gp2;
+                        lr = gr;
                         perm = nullptr;
                     }
-                    run_list(li, counts[c], c, false, lp, lp2, perm);
+                    run_list(nullptr, lr, counts[c], c, false, perm);
                     continue;
                 }
                 if (counts[c] == 0) continue;
@@ -708,8 +707,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     CG_CUDA(cudaEventRecord(E.ev[12], x.s));
                     CG_CUDA(cudaStreamWaitEvent(streams[k], E.ev[12], 0));
                 }
-                run_list_on(items, counts[c], c, false, lparts + (size_t)c * cap, lparts2 + (size_t)c * cap, perm,
-                            streams[k], k);
+                run_list_on(nullptr, recs, counts[c], c, false, perm, streams[k], k);
             }
             if (conc)
                 for (int k = 1; k < 4 && k < nlaunched; ++k) {

@@ -128,9 +128,12 @@ __global__ void k_row_crn(RowSetupArgs a, const double* __restrict__ L) {
 
 enum : int { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2, ST_FINISH = 3 };
 
+constexpr int kGsParts = 16;  // parts held in GroupShared (>= kRecMaxParts)
+
 struct GroupShared {
     unsigned long long plan;  // current plan index
     unsigned long long hi;    // end of current item (exclusive)
+    double lbk;   // the plan's service bound: sojourns below it never reach the p95
     int row;
     int used;   // GPUs of the current count vector
     int dp;
@@ -138,36 +141,51 @@ struct GroupShared {
     int has_item;
     int dp_enum;  // replicas of the current count vector
     int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
-    unsigned char pshape[8], pcount[8];
+    int qi;       // future-bound blocks of the plan (SimArgs::qtab)
+    unsigned char pshape[kGsParts], pcount[kGsParts];
     unsigned char counts[kMaxShapes];
 };
 
-// A plan's shape multiset packed by the filter (which enumerates the plan
-// anyway), so acquiring it needs no unranking.  Word 0: bits 0-2 number of
-// parts when it is <= 4 (0 otherwise), 3-11 GPUs used, then parts 0..3 (5 bits
-// shape index + 8 bits count each).  Word 1: bits 0-3 number of parts when it
-// is <= 8 (0 = not packable: unrank), then parts 4..7 in the same 13-bit form.
-struct PackedParts {
-    unsigned long long w0, w1;
-};
-__device__ __forceinline__ PackedParts encode_parts(const unsigned char* c, int S, int used) {
-    PackedParts v{0ull, 0ull};
+// ItemRec part stream (cg_kernels.h): header (np, used) then 13-bit parts.
+__device__ __forceinline__ void encode_rec(ItemRec& r, const unsigned char* c, int S, int used) {
+    unsigned long long w0 = 0ull, w1 = 0ull, w2 = 0ull;
     int np = 0;
     for (int s = 0; s < S; ++s) {
         if (!c[s]) continue;
-        if (np == 8) return PackedParts{0ull, 0ull};
+        if (np == kRecMaxParts) {
+            np = -1;
+            break;
+        }
         const unsigned long long f = (unsigned long long)s | ((unsigned long long)c[s] << 5);
-        if (np < 4) v.w0 |= f << (12 + 13 * np);
-        else v.w1 |= f << (4 + 13 * (np - 4));
+        const int off = 13 + 13 * np;
+        const int sh = off & 63;
+        const unsigned long long lo = f << sh, hi = sh > 51 ? f >> (64 - sh) : 0ull;
+        if (off < 64) {
+            w0 |= lo;
+            w1 |= hi;
+        } else if (off < 128) {
+            w1 |= lo;
+            w2 |= hi;
+        } else {
+            w2 |= lo;
+        }
         ++np;
     }
-    if (used > 511) return PackedParts{0ull, 0ull};
-    v.w0 |= (unsigned long long)(np <= 4 ? np : 0) | ((unsigned long long)used << 3);
-    v.w1 |= (unsigned long long)np;
-    return v;
+    if (np < 0 || used > 511) w0 = w1 = w2 = 0ull;
+    else w0 |= (unsigned long long)np | ((unsigned long long)used << 4);
+    r.w[0] = w0;
+    r.w[1] = w1;
+    r.w[2] = w2;
 }
-__device__ __forceinline__ unsigned part_field(const PackedParts& v, int q) {
-    return q < 4 ? (unsigned)(v.w0 >> (12 + 13 * q)) & 0x1fffu : (unsigned)(v.w1 >> (4 + 13 * (q - 4))) & 0x1fffu;
+__device__ __forceinline__ unsigned rec_part(unsigned long long w0, unsigned long long w1, unsigned long long w2,
+                                             int q) {
+    const int off = 13 + 13 * q;
+    const int sh = off & 63;
+    const unsigned long long a = off < 64 ? w0 : (off < 128 ? w1 : w2);
+    const unsigned long long b = off < 64 ? w1 : w2;
+    unsigned long long v = a >> sh;
+    if (sh > 51) v |= b << (64 - sh);
+    return (unsigned)v & 0x1fffu;
 }
 
 // MODE: 0 = plan-index ranges (smem rings), 1 = explicit plan list (smem
@@ -271,24 +289,32 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
             return;
         }
         const unsigned long long slot = a.perm ? (unsigned long long)a.perm[it] : it;
-        const unsigned long long item = a.items[slot];
-        const unsigned long long pk = a.parts ? a.parts[slot] : 0ull;
+        unsigned long long item, w0 = 0ull, w1 = 0ull, w2 = 0ull;
+        if (a.recs) {
+            const ItemRec& rec = a.recs[slot];
+            item = rec.item;
+            w0 = rec.w[0];
+            w1 = rec.w[1];
+            w2 = rec.w[2];
+        } else {
+            item = a.items[slot];
+        }
         const int row = (int)(item >> kItemPlanBits);
         const unsigned long long plan = item & kItemPlanMask;
         const RowDesc& rd = a.rows[row];
         const PlanSpace& sp = a.spaces[rd.space];
         int dp = 0;
-        const int np = (int)(pk & 7ull);
+        const int np = (int)(w0 & 15ull);
         if (np > 0) {
             for (int s = 0; s < sp.S; ++s) gs.counts[s] = 0;
             for (int q = 0; q < np; ++q) {
-                const unsigned v = (unsigned)(pk >> (12 + 13 * q)) & 0x1fffu;
+                const unsigned v = rec_part(w0, w1, w2, q);
                 gs.pshape[q] = (unsigned char)(v & 31u);
                 gs.pcount[q] = (unsigned char)(v >> 5);
                 gs.counts[v & 31u] = (unsigned char)(v >> 5);
                 dp += (int)(v >> 5);
             }
-            gs.used = (int)((pk >> 3) & 511ull);
+            gs.used = (int)((w0 >> 4) & 511ull);
         } else {
             gs.used = unrank_plan(sp, plan, gs.counts);
             for (int s = 0; s < sp.S; ++s) dp += gs.counts[s];
@@ -759,43 +785,53 @@ struct LaneTraits {
 };
 
 // Claims work item `it` into gs; false when the item is rejected (an unstable
-// seed, or a service bound above the live bound).
+// seed, or a service bound above the live bound).  Filtered items (recs)
+// carry their parts and service bound, so a claim is one round of
+// independent loads (the record) and one dependent one (the live bound and
+// the plan's future-bound blocks, SimArgs::qtab).
 __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long it) {
     const unsigned long long slot = a.perm ? (unsigned long long)a.perm[it] : it;
-    const unsigned long long item = a.items[slot];
-    PackedParts pk{0ull, 0ull};
-    if (a.parts && a.parts2) {
-        pk.w0 = a.parts[slot];
-        pk.w1 = a.parts2[slot];
+    unsigned long long item, w0 = 0ull, w1 = 0ull, w2 = 0ull;
+    double lb = 0.0;
+    const bool rec = a.recs != nullptr;
+    if (rec) {
+        const ItemRec& r = a.recs[slot];
+        item = r.item;
+        w0 = r.w[0];
+        w1 = r.w[1];
+        w2 = r.w[2];
+        lb = r.lb;
+    } else {
+        item = a.items[slot];
     }
     const int row = (int)(item >> kItemPlanBits);
     const unsigned long long plan = item & kItemPlanMask;
     const RowDesc& rd = a.rows[row];
     const PlanSpace& sp = a.spaces[rd.space];
     const long long rb = (long long)row * kMaxShapes;
-    int np = (int)(pk.w1 & 15ull);
+    int np = (int)(w0 & 15ull);
     int dp = 0, used = 0;
     if (np > 0) {
         for (int q = 0; q < np; ++q) {
-            const unsigned v = part_field(pk, q);
+            const unsigned v = rec_part(w0, w1, w2, q);
             gs.pshape[q] = (unsigned char)(v & 31u);
             gs.pcount[q] = (unsigned char)(v >> 5);
             dp += (int)(v >> 5);
         }
-        used = (int)((pk.w0 >> 3) & 511ull);
+        used = (int)((w0 >> 4) & 511ull);
     } else {
         used = unrank_plan(sp, plan, gs.counts);
         for (int s = 0; s < sp.S; ++s) {
             const int c = gs.counts[s];
             if (!c) continue;
-            if (np < 8) {
+            if (np < kGsParts) {
                 gs.pshape[np] = (unsigned char)s;
                 gs.pcount[np] = (unsigned char)c;
             }
             ++np;
             dp += c;
         }
-        if (np > 8) np = 0;  // counts[] stay authoritative
+        if (np > kGsParts) np = 0;  // counts[] stay authoritative
     }
     if (a.check_stable) {  // seeds are not pre-filtered (costmodel.cpp:366-376)
         double capacity = 0.0;
@@ -807,28 +843,46 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
             capacity = __dadd_rn(capacity, __ddiv_rn((double)c, a.tab.mean_service[rb + sh]));
         }
         if (rd.rate >= capacity) return false;
-    } else if (a.prune) {
-        const double U = __longlong_as_double(
-            (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
+    }
+    if (!rec) {  // the service bound (k_plan_filter computes it for filtered items)
         const double o_k = a.tab.O[(long long)row * a.tab.ld + a.kstar];
         const double t_max = a.tab.T[(long long)row * a.tab.ld + a.n_req - 1];
-        double lb = __longlong_as_double(0x7ff0000000000000ll);
+        double m = __longlong_as_double(0x7ff0000000000000ll);
         for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
             const int sh = np > 0 ? gs.pshape[q] : s;
             if (np == 0 && !gs.counts[s]) continue;
             const double v = a.tab.prefill[rb + sh] + o_k * a.tab.decode[rb + sh];
-            lb = v < lb ? v : lb;
+            m = v < m ? v : m;
         }
-        if (lb * (1.0 - 1e-12) - 1e-12 * t_max > U) {
+        lb = m * (1.0 - 1e-12) - 1e-12 * t_max;
+    }
+    if (a.prune && !a.check_stable) {
+        const double U = __longlong_as_double(
+            (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
+        if (lb > U) {
             atomicAdd(&a.counters[CTR_BOUND], 1ull);
             return false;
         }
+    }
+    int qi = 0;
+    if (a.prune && a.qtab && a.tab.nc > 0) {
+        const unsigned short* qt = a.qtab + ((long long)row * (a.N + 1) + used) * kMaxShapes;
+        qi = 1 << 30;
+        for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
+            const int sh = np > 0 ? gs.pshape[q] : s;
+            if (np == 0 && !gs.counts[s]) continue;
+            const int v = qt[sh];
+            qi = v < qi ? v : qi;
+        }
+        qi = qi == (1 << 30) ? 0 : qi;
     }
     gs.nparts = np;
     gs.row = row;
     gs.plan = plan;
     gs.dp = dp;
     gs.used = used;
+    gs.qi = qi;
+    gs.lbk = lb;
     return true;
 }
 
@@ -866,6 +920,8 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
 
     int status = ST_NEED;
     int row = 0, dp = 0, gpus = 0, k = 0, ab = 0, qi = 0;
+    int ns = 0;          // sojourns recorded in the plan's scratch column (those >= lbk)
+    double lbk = 0.0;    // the plan's service bound: smaller sojourns are never the p95
     unsigned long long plan = 0;
     bool ovf = false;
     unsigned lazy = 0;
@@ -954,6 +1010,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     for (int r = 0; r < R; ++r) mcur |= (gl * R + r < dp) ? (1u << r) : 0u;
                     k = 0;
                     ab = 0;
+                    ns = 0;
+                    qi = gs.qi;
+                    lbk = gs.lbk;
                     ovf = false;
                     lazy = 0;
                     tq = *reinterpret_cast<const double2*>(Trow);
@@ -967,14 +1026,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             __syncwarp();
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
-        {
-            U = __shfl_sync(FULL, U, gshift);  // one bound per group (leader's)
-            const bool fresh = need && status == ST_RUN;
-            if (a.prune && a.tab.nc > 0 && __any_sync(FULL, fresh)) {
-                const int q = future_blocks<W>(a, gs, row, fresh, U, gl, gshift, wmask, 0);
-                if (fresh) qi = q;
-            }
-        }
+        U = __shfl_sync(FULL, U, gshift);  // one bound per group (leader's)
 
         // ---- phase B: UNROLL request-steps per running plan, as pairs (rows
         // and k are even-aligned) with the next pair's arrivals/outputs
@@ -1129,7 +1181,11 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
                 }
                 ab += (me && soj > U) ? 1 : 0;
-                if (me) scratch[k] = soj;
+                // only sojourns >= the service bound can be among the K largest
+                const bool keep = me && !(soj < lbk);
+                if (keep) scratch[ns] = soj;
+                if (W == 1) ns += keep ? 1 : 0;
+                else ns += ((__ballot_sync(FULL, keep) >> gshift) & wmask) ? 1 : 0;
                 const unsigned rb = me ? (1u << rr) : 0u;
                 mcur = (mn & ~rb) | ((fin <= tn1) ? rb : 0u);
             }
@@ -1162,8 +1218,10 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 tot += __shfl_xor_sync(FULL, tot, off);
                 ov |= __shfl_xor_sync(FULL, ov, off);
             }
-            bool urefresh = false;
             if (status == ST_RUN) {
+                // qi comes from the launch's bound snapshot (>= the live bound):
+                // sojourns counted against any of the bounds seen exceed the
+                // smallest of them, itself a latency found at <= gpus
                 const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
                 if (ov) {
                     if (gl == 0) {
@@ -1177,18 +1235,11 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                     steps += k;
                     status = ST_NEED;
                 } else if (a.prune) {
-                    const double U2 = __longlong_as_double(
+                    U = __longlong_as_double(
                         (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
-                    urefresh = U2 < U;
-                    U = U2;
                 }
             }
             U = __shfl_sync(FULL, U, gshift);
-            urefresh = __shfl_sync(FULL, urefresh ? 1 : 0, gshift) != 0;
-            if (a.tab.nc > 0 && __any_sync(FULL, urefresh)) {
-                const int q = future_blocks<W>(a, gs, row, urefresh, U, gl, gshift, wmask, qi);
-                if (urefresh) qi = q;
-            }
             if (status == ST_NEED && gl == 0) gs.status = ST_NEED;
         }
 
@@ -1204,6 +1255,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             bool sel = false;
             if (status == ST_FINISH) {
                 steps += k;
+                ov |= ns < a.K ? 1 : 0;  // cannot happen (lbk <= p95); the DEEP re-run keeps every sojourn
                 if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
@@ -1221,7 +1273,8 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 const int ldr = __ffs(fm) - 1;
                 fm &= fm - 1u;
                 const double* col = a.scratch + (gwarp * G + ldr / W) * (long long)a.sld;
-                const unsigned long long xb = group_kth_largest<32, true>(col, n_req, a.K, lane, FULL, 0, hist);
+                const int nsel = __shfl_sync(FULL, ns, ldr);
+                const unsigned long long xb = group_kth_largest<32, true>(col, nsel, a.K, lane, FULL, 0, hist);
                 if (lane == ldr) {
                     full += 1;
                     const long long base = (long long)row * (a.N + 1);
@@ -1388,6 +1441,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
         }
         int cls = -1;
         unsigned long long key = 0;
+        double lbs = 0.0;  // the listed plan's service bound (ItemRec::lb)
         if (live) {
             // Stability (costmodel.cpp:366-376): rate < sum over parts of cnt /
             // mean_service, summed in parts order.  Fast test first: each term
@@ -1421,6 +1475,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 ++stable;
                 bool keep = true;
                 lb = lb * (1.0 - 1e-12) - 1e-12 * t_max;
+                lbs = lb;
                 // coarse order key, likely-good plans first: the service bound,
                 // or (sort_key 1) the heuristic estimate service bound / (1 - utilisation)
                 // order heuristics (results never depend on them): 1 fast-shape
@@ -1466,10 +1521,11 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 base = __shfl_sync(peers, base, leader);
                 const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
                 if (slot < a.list_cap) {
-                    a.lists[cls][slot] = ((unsigned long long)row << kItemPlanBits) | p;
-                    const PackedParts pk = encode_parts(c, sp.S, used);
-                    a.parts[cls][slot] = pk.w0;
-                    a.parts2[cls][slot] = pk.w1;
+                    ItemRec r;
+                    r.item = ((unsigned long long)row << kItemPlanBits) | p;
+                    encode_rec(r, c, sp.S, used);
+                    r.lb = lbs;
+                    a.recs[cls][slot] = r;
                     a.keys[cls][slot] = key;
                 }
             }
@@ -1478,6 +1534,40 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
     if (a.pilot_only) return;
     if (stable) atomicAdd(&a.counters[CTR_STABLE], stable);
     if (skipped) atomicAdd(&a.counters[CTR_BOUND], skipped);
+}
+
+// Future-bound snapshot: per (row, budget g, shape s) the number of leading
+// output-ranked request blocks i whose smallest output Pv[row][i] still gives
+// a service lower bound above ub[row][g] on shape s -- the same predicate the
+// plan-level bound applies to min over the plan's shapes, which is the
+// minimum of these per-shape counts (the predicate is monotone in the
+// bound, and min_s commutes with the monotone margin transform).  Pv is
+// non-increasing in i, so the qualifying blocks form a prefix: binary search.
+__global__ void k_fut_snapshot(FutSnapArgs a) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long cells = (long long)a.nrows * (a.N + 1);
+    if (t >= cells * kMaxShapes) return;
+    const long long cell = t / kMaxShapes;
+    const int s = (int)(t % kMaxShapes);
+    const int row = (int)(cell / (a.N + 1));
+    const PlanSpace& sp = a.spaces[a.rows[row].space];
+    unsigned short q = 0;
+    const double U = __longlong_as_double((long long)*(volatile const unsigned long long*)&a.ub[cell]);
+    if (s < sp.S && a.tab.nc > 0 && U < __longlong_as_double(0x7ff0000000000000ll)) {
+        const long long rb = (long long)row * kMaxShapes;
+        const double p = a.tab.prefill[rb + s], d = a.tab.decode[rb + s];
+        const double t_max = a.tab.T[(long long)row * a.tab.ld + a.n_req - 1];
+        const double* Pv = a.tab.Pv + (long long)row * a.tab.nc;
+        int lo = 0, hi = a.tab.nc;  // answer in [lo, hi]: blocks [0, lo) qualify, [hi, nc) do not
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const double v = p + Pv[mid] * d;
+            if (v * (1.0 - 1e-12) - 1e-12 * t_max > U) lo = mid + 1;
+            else hi = mid;
+        }
+        q = (unsigned short)lo;
+    }
+    a.qtab[t] = q;
 }
 
 __global__ void k_pilot_lists(PilotArgs a) {
@@ -1619,6 +1709,14 @@ void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t 
         }
     }
     throw EngineError(101, "unsupported JSQ kernel class");
+}
+
+void launch_fut_snapshot(const FutSnapArgs& a, cudaStream_t s, int* launches) {
+    const long long work = (long long)a.nrows * (a.N + 1) * kMaxShapes;
+    if (work == 0 || !a.qtab) return;
+    k_fut_snapshot<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
 }
 
 void launch_pilot_lists(const PilotArgs& a, cudaStream_t s, int* launches) {
