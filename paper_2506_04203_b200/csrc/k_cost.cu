@@ -281,7 +281,7 @@ __device__ __forceinline__ int future_blocks(const SimArgs& a, const GroupShared
 // are seeds / overflow re-runs.  The service-time bound is re-checked against
 // the live bound (it tightens while the kernel runs).
 template <int MODE>
-__device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
+__device__ void acquire_plan(const SimArgs& a, GroupShared& gs, unsigned long long& bound) {
     while (true) {
         const unsigned long long it = atomicAdd(a.item_counter, 1ull);
         if (it >= a.nitems) {
@@ -339,7 +339,7 @@ __device__ void acquire_plan(const SimArgs& a, GroupShared& gs) {
             const double U = __longlong_as_double(
                 (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gs.used]);
             if (service_bound(a, row, sp, gs.counts) > U) {
-                atomicAdd(&a.counters[CTR_BOUND], 1ull);
+                ++bound;
                 continue;
             }
         }
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
         nd[r] = avail[r] = pre[r] = dec[r] = 0.0;
         cnt[r] = head[r] = tail[r] = 0;
     }
-    unsigned long long steps = 0, full = 0, pruned = 0;
+    unsigned long long steps = 0, full = 0, pruned = 0, bound = 0;
     int qi = 0;  // output-ranked blocks whose requests all exceed U on service alone
     const double INF = __longlong_as_double((long long)kInfBits);
 
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
         // ---- phase A: groups without a plan acquire one
         const bool need = status == ST_NEED;
         if (__any_sync(FULL, need)) {
-            if (need && gl == 0) acquire_plan<MODE>(a, gs);
+            if (need && gl == 0) acquire_plan<MODE>(a, gs, bound);
             __syncwarp();
             if (need) {
                 status = gs.status;
@@ -747,6 +747,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
     }
     // per-lane counters -> global (leaders only to avoid double counting)
     if (gl == 0) {
+        count_add(&a.counters[CTR_BOUND], bound);
         count_add(&a.counters[CTR_STEPS], steps);
         count_add(&a.counters[a.seeds ? CTR_SEED : CTR_FULL], full);
         count_add(&a.counters[a.seeds ? CTR_SEED : CTR_PRUNED], pruned);
@@ -777,9 +778,14 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
 template <int W, int R>
 struct LaneTraits {
     static constexpr int G = 32 / W;
-    static constexpr int CAP = R <= 4 ? 32 : 16;
+    // waiting-job ring slots per replica (W = 1, R = 8: 8 slots keep three
+    // 128-thread blocks per SM within shared memory); deeper queues overflow
+    // to the DEEP re-run.  (Four blocks per SM -- 128 registers, half the
+    // slots -- measured slower: C3 K4 746 -> 795 ms.)
+    static constexpr int CAP = R <= 4 ? 32 : (W == 1 ? 8 : 16);
+    static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
-    static constexpr size_t pd_bytes = (size_t)2 * R * 32 * sizeof(double);
+    static constexpr size_t pd_bytes = (size_t)3 * R * 32 * sizeof(double);  // prefill, decode, head finish
     static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
     static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + hist_bytes + G * sizeof(GroupShared);
 };
@@ -789,8 +795,7 @@ struct LaneTraits {
 // carry their parts and service bound, so a claim is one round of
 // independent loads (the record) and one dependent one (the live bound and
 // the plan's future-bound blocks, SimArgs::qtab).
-__device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long it) {
-    const unsigned long long slot = a.perm ? (unsigned long long)a.perm[it] : it;
+__device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long slot, unsigned long long& bound) {
     unsigned long long item, w0 = 0ull, w1 = 0ull, w2 = 0ull;
     double lb = 0.0;
     const bool rec = a.recs != nullptr;
@@ -860,7 +865,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
         const double U = __longlong_as_double(
             (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + used]);
         if (lb > U) {
-            atomicAdd(&a.counters[CTR_BOUND], 1ull);
+            ++bound;
             return false;
         }
     }
@@ -889,7 +894,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
 constexpr unsigned kLaneCheck = 32;  // request-steps between exact-bound prune checks
 
 template <int W, int R>
-__global__ void __launch_bounds__(128) k_lane(SimArgs a) {
+__global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimArgs a) {
     using TR = LaneTraits<W, R>;
     constexpr int G = TR::G;
     constexpr int CAP = TR::CAP;
@@ -906,6 +911,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
     unsigned short* ring = reinterpret_cast<unsigned short*>(wbase);
     double* pre_s = reinterpret_cast<double*>(wbase + TR::ring_bytes);
     double* dec_s = pre_s + R * 32;
+    double* nd_s = dec_s + R * 32;  // finish time of each replica's head job (INF: none)
     unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
     GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::hist_bytes);
     GroupShared& gs = gsa[gid];
@@ -931,7 +937,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
     const double* Orow = a.tab.O;
     // arrivals / outputs of the pair holding step k and of the next pair (prefetched)
     double2 tq = make_double2(0.0, 0.0), oq = tq, tq2 = tq, oq2 = tq;
-    double avail[R], nd[R];
+    // per replica: avail = finish of its last job, prev = finish of the job
+    // before it (0 = none); the head job's finish lives in shared memory (nd_s)
+    double avail[R], prev[R];
     // W == 1: output tokens of the job at the ring head, loaded one pop ahead
     // (the lanes' rows differ, so a load at pop time would stall on L2)
     constexpr bool HO = W == 1;
@@ -940,11 +948,11 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         avail[r] = INF;
-        nd[r] = INF;
+        prev[r] = INF;
         ho[r] = 0.0;
         ht[r] = 0;
     }
-    unsigned long long steps = 0, full = 0, pruned = 0;
+    unsigned long long steps = 0, full = 0, pruned = 0, bound = 0;
 
     for (unsigned it = 0;; ++it) {
         // ---- phase A: groups without a plan claim one (one atomic per round)
@@ -961,7 +969,8 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 if (want) {
                     const unsigned long long item = base + __popc(m & ((1u << lane) - 1u));
                     if (item >= a.nitems) gs.status = ST_DONE;
-                    else if (lane_take(a, gs, item)) gs.status = ST_RUN;
+                    else if (lane_take(a, gs, a.perm ? (unsigned long long)a.perm[item] : item, bound))
+                        gs.status = ST_RUN;
                     else again = true;
                 }
                 want = again;
@@ -984,9 +993,10 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
-                        nd[r] = INF;
+                        nd_s[r * 32 + lane] = INF;
                         ht[r] = 0;
                         avail[r] = INF;
+                        prev[r] = INF;
                         if (j < dp) {
                             if (np > 0) {
                                 while (j >= cum) {
@@ -1003,6 +1013,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                             pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
                             dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
                             avail[r] = 0.0;
+                            prev[r] = 0.0;
                         }
                     }
                     mcur = 0;  // every replica starts idle (avail 0 <= T[0])
@@ -1040,6 +1051,9 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             unsigned mn = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) mn |= (avail[r] <= tn1) ? (1u << r) : 0u;
+            // a sojourn counts toward the prune test only while the FIFOs are
+            // intact (no ring overflow in the group so far)
+            const bool intact = W == 1 ? !ovf : ((__ballot_sync(FULL, ovf) >> gshift) & wmask) == 0u;
             bool idle;
             int wlane;
             if (W == 1) {
@@ -1056,85 +1070,92 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             // block so its shared-memory loads and fp64 chain overlap it
             const int pidx0 = (rr > 0 ? rr : 0) * 32 + lane;
             double fin = __dadd_rn(__dadd_rn(t, pre_s[pidx0]), __dmul_rn(o, dec_s[pidx0]));
+            double start = t;
             unsigned H = 0;
-            // W == 1: each lane is its own plan, plain divergent control flow
-            // (no warp vote on the step path)
+            bool one = false;  // count-1 dispatch: the replica holds only its last job
             if (W == 1 ? busy : __any_sync(FULL, busy)) {
-                if (busy && lazy) {
+                // Every replica busy.  A replica with exactly one job in system
+                // (every earlier job finished: prev <= t) has the minimum count,
+                // so the lowest such replica is the reference's argmin
+                // (costmodel.cpp:262-276) -- no FIFO walk needed.
+                unsigned m1 = 0;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {  // selects, no per-replica branch
-                        const bool lz = (lazy >> r) & 1u;
-                        nd[r] = lz ? avail[r] : nd[r];
-                        ht[r] = lz ? ((ht[r] & 0xffff0000u) | (ht[r] >> 16)) : ht[r];
+                for (int r = 0; r < R; ++r) m1 |= (prev[r] <= t) ? (1u << r) : 0u;
+                m1 = busy ? m1 : 0u;
+                bool has1;
+                if (W == 1) {
+                    has1 = m1 != 0u;
+                } else {
+                    const unsigned g1 = (__ballot_sync(FULL, m1 != 0u) >> gshift) & wmask;
+                    has1 = g1 != 0u;
+                    if (busy && has1) wlane = __ffs(g1) - 1;
+                }
+                if (busy && has1) {
+                    rr = __ffs(m1) - 1;
+                    one = true;
+                }
+                const bool slow = busy && !has1;
+                if (W == 1 ? slow : __any_sync(FULL, slow)) {
+                    // every replica holds >= 2 jobs: materialise the lazy FIFOs,
+                    // pop up to t, then the (in-system count, index) minimum
+                    if (slow && lazy) {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const bool lz = (lazy >> r) & 1u;
+                            if (lz) nd_s[r * 32 + lane] = avail[r];
+                            ht[r] = lz ? ((ht[r] & 0xffff0000u) | (ht[r] >> 16)) : ht[r];
+                        }
+                        lazy = 0;
                     }
-                    lazy = 0;
-                }
-                bool dep[R];
-                bool anydep = false;
+                    unsigned dep = 0;
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    dep[r] = busy && nd[r] <= t;
-                    anydep |= dep[r];
-                }
-                while (W == 1 ? anydep : __any_sync(FULL, anydep)) {
-                    anydep = false;
+                    for (int r = 0; r < R; ++r) dep |= (slow && nd_s[r * 32 + lane] <= t) ? (1u << r) : 0u;
+                    while (W == 1 ? dep != 0u : __any_sync(FULL, dep != 0u)) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        if (R <= 4) {  // few replicas: straight-line selects, predicated loads
+                        for (int r = 0; r < R; ++r) {
+                            if (!((dep >> r) & 1u)) continue;
                             const unsigned h = ht[r] & 0xffffu;
                             const unsigned tl = ht[r] >> 16;
-                            const bool pop = dep[r] && h != tl;
-                            double oh = 0.0;
-                            if (HO) oh = ho[r];
-                            else if (pop) oh = Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
-                            const double nx = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
-                                                        __dmul_rn(oh, dec_s[r * 32 + lane]));
-                            nd[r] = pop ? nx : (dep[r] ? INF : nd[r]);
-                            const unsigned h1 = (h + 1u) & 0xffffu;
-                            ht[r] = pop ? ((ht[r] & 0xffff0000u) | h1) : ht[r];
-                            if (HO && pop && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
-                            dep[r] = dep[r] && nd[r] <= t;
-                            anydep |= dep[r];
-                        } else if (dep[r]) {
-                            const unsigned h = ht[r] & 0xffffu;
-                            const unsigned tl = ht[r] >> 16;
-                            const bool more = h != tl;  // the head job enters service
+                            const bool more = h != tl;  // the head waiting job enters service
                             double oh = 0.0;
                             if (HO) oh = ho[r];
                             else if (more) oh = Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
-                            const double nx = __dadd_rn(__dadd_rn(nd[r], pre_s[r * 32 + lane]),
+                            const double ndr = nd_s[r * 32 + lane];
+                            const double nx = __dadd_rn(__dadd_rn(ndr, pre_s[r * 32 + lane]),
                                                         __dmul_rn(oh, dec_s[r * 32 + lane]));
-                            nd[r] = more ? nx : INF;
+                            const double nn = more ? nx : INF;
+                            nd_s[r * 32 + lane] = nn;
                             const unsigned h1 = (h + 1u) & 0xffffu;
                             ht[r] = more ? ((ht[r] & 0xffff0000u) | h1) : ht[r];
                             if (HO && more && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
-                            dep[r] = nd[r] <= t;
-                            anydep |= dep[r];
+                            dep = (nn <= t) ? dep : (dep & ~(1u << r));
                         }
                     }
-                }
-                // (in-system count << 9 | replica) minimum, as a tree
-                unsigned kk[R];
+                    // (in-system count << 9 | replica) minimum, as a tree
+                    unsigned kk[R];
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int j = gl * R + r;
-                    const unsigned c = (((ht[r] >> 16) - ht[r]) & 0xffffu) + (nd[r] < INF ? 1u : 0u);
-                    kk[r] = (j < dp) ? ((c << 9) | (unsigned)j) : 0xffffffffu;
-                }
+                    for (int r = 0; r < R; ++r) {
+                        const int j = gl * R + r;
+                        const unsigned c = (((ht[r] >> 16) - ht[r]) & 0xffffu) + (nd_s[r * 32 + lane] < INF ? 1u : 0u);
+                        kk[r] = (j < dp) ? ((c << 9) | (unsigned)j) : 0xffffffffu;
+                    }
 #pragma unroll
-                for (int w = 1; w < R; w <<= 1)
+                    for (int w = 1; w < R; w <<= 1)
 #pragma unroll
-                    for (int r = 0; r + w < R; r += 2 * w) kk[r] = kk[r + w] < kk[r] ? kk[r + w] : kk[r];
-                unsigned key = busy ? kk[0] : 0xffffffffu;
+                        for (int r = 0; r + w < R; r += 2 * w) kk[r] = kk[r + w] < kk[r] ? kk[r + w] : kk[r];
+                    unsigned key = slow ? kk[0] : 0xffffffffu;
 #pragma unroll
-                for (int off = W / 2; off > 0; off >>= 1) {
-                    const unsigned v = __shfl_xor_sync(FULL, key, off);
-                    key = v < key ? v : key;
+                    for (int off = W / 2; off > 0; off >>= 1) {
+                        const unsigned v = __shfl_xor_sync(FULL, key, off);
+                        key = v < key ? v : key;
+                    }
+                    if (slow) {
+                        const int win = (int)(key & 511u);
+                        wlane = win / R;
+                        rr = win % R;
+                    }
                 }
                 if (busy) {
-                    const int win = (int)(key & 511u);
-                    wlane = win / R;
-                    rr = win % R;
                     // avail / ring state of replica rr: select tree on rr's bits
                     double av[R];
                     unsigned hv[R];
@@ -1153,17 +1174,23 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                         }
                     }
                     H = hv[0];
-                    // start = avail of the chosen replica (> t: std::max(t, avail))
+                    start = av[0];  // > t: std::max(t, avail)
                     const int pidx = rr * 32 + lane;
-                    fin = __dadd_rn(__dadd_rn(av[0], pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
+                    fin = __dadd_rn(__dadd_rn(start, pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
                 }
             }
             const bool me = run && gl == wlane;
             const double soj = __dsub_rn(fin, t);
             {
-                // predicated on `me` throughout (no branch).  Idle: the FIFO now
-                // holds just this job (lazy reset; H = 0 is an empty ring).
-                // Busy: the job joins the queue.
+                // predicated on `me` throughout.  Idle: the FIFO now holds just
+                // this job (lazy reset; H = 0 is an empty ring).  Count-1: the
+                // job in service (finishing at start) and this one waiting --
+                // the ring restarts empty.  Otherwise the job joins the queue.
+                if (me && one) {
+                    H = (H & 0xffff0000u) | (H >> 16);
+                    nd_s[rr * 32 + lane] = start;
+                    lazy &= ~(1u << rr);
+                }
                 const bool push = me && !idle;
                 const bool first = push && ((H >> 16) == (H & 0xffffu));  // the ring was empty
                 if (push) ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
@@ -1173,6 +1200,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const bool hit = me && r == rr;
+                    prev[r] = hit ? avail[r] : prev[r];
                     avail[r] = hit ? fin : avail[r];
                     ht[r] = hit ? H : ht[r];
                 }
@@ -1180,7 +1208,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
 #pragma unroll
                     for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
                 }
-                ab += (me && soj > U) ? 1 : 0;
+                ab += (me && intact && soj > U) ? 1 : 0;
                 // only sojourns >= the service bound can be among the K largest
                 const bool keep = me && !(soj < lbk);
                 if (keep) scratch[ns] = soj;
@@ -1223,15 +1251,15 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
                 // sojourns counted against any of the bounds seen exceed the
                 // smallest of them, itself a latency found at <= gpus
                 const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
-                if (ov) {
+                if (a.prune && tot + fut >= a.K) {  // tot: sojourns of intact steps only
+                    pruned += 1;
+                    steps += k;
+                    status = ST_NEED;
+                } else if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
                         if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
                     }
-                    steps += k;
-                    status = ST_NEED;
-                } else if (a.prune && tot + fut >= a.K) {
-                    pruned += 1;
                     steps += k;
                     status = ST_NEED;
                 } else if (a.prune) {
@@ -1256,13 +1284,13 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
             if (status == ST_FINISH) {
                 steps += k;
                 ov |= ns < a.K ? 1 : 0;  // cannot happen (lbk <= p95); the DEEP re-run keeps every sojourn
-                if (ov) {
+                if (a.prune && tot >= a.K) {
+                    pruned += 1;
+                } else if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
                         if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)row << kItemPlanBits) | plan;
                     }
-                } else if (a.prune && tot >= a.K) {
-                    pruned += 1;
                 } else {
                     sel = true;
                 }
@@ -1299,6 +1327,7 @@ __global__ void __launch_bounds__(128) k_lane(SimArgs a) {
         }
     }
     if (gl == 0) {
+        count_add(&a.counters[CTR_BOUND], bound);
         count_add(&a.counters[CTR_STEPS], steps);
         count_add(&a.counters[a.seeds ? CTR_SEED : CTR_FULL], full);
         count_add(&a.counters[a.seeds ? CTR_SEED : CTR_PRUNED], pruned);
@@ -1665,13 +1694,42 @@ int class_for_dp(int dpmax) {
     return -1;
 }
 
+static void launch_sim_impl(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
+                            int* grid_out);
+
+// Diagnostic (CG_TRACE_K4=1): per launch, the class, items, request-steps,
+// completed / pruned plans and the launch time (synchronising: not for timing
+// runs).
 void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out) {
     static const bool trace = std::getenv("CG_TRACE_K4") != nullptr;
-    if (trace && a.nitems > 0) {
-        std::fprintf(stderr, "[k4] cls=%d mode=%d items=%llu\n", cls, mode, (unsigned long long)a.nitems);
-        std::fflush(stderr);
+    if (!trace || a.nitems == 0 || !a.counters) {
+        launch_sim_impl(a, cls, mode, sm_count, s, launches, grid_out);
+        return;
     }
+    unsigned long long c0[CTR_COUNT], c1[CTR_COUNT];
+    CG_CUDA(cudaStreamSynchronize(s));
+    CG_CUDA(cudaMemcpy(c0, a.counters, sizeof(c0), cudaMemcpyDeviceToHost));
+    cudaEvent_t e0, e1;
+    CG_CUDA(cudaEventCreate(&e0));
+    CG_CUDA(cudaEventCreate(&e1));
+    CG_CUDA(cudaEventRecord(e0, s));
+    launch_sim_impl(a, cls, mode, sm_count, s, launches, grid_out);
+    CG_CUDA(cudaEventRecord(e1, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    CG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    CG_CUDA(cudaMemcpy(c1, a.counters, sizeof(c1), cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::fprintf(stderr, "[k4] cls=%d mode=%d seeds=%d items=%llu steps=%llu full=%llu pruned=%llu bound=%llu ms=%.3f\n",
+                 cls, mode, a.seeds, (unsigned long long)a.nitems, c1[CTR_STEPS] - c0[CTR_STEPS],
+                 c1[CTR_FULL] - c0[CTR_FULL], c1[CTR_PRUNED] - c0[CTR_PRUNED], c1[CTR_BOUND] - c0[CTR_BOUND], ms);
+    std::fflush(stderr);
+}
+
+static void launch_sim_impl(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
+                            int* grid_out) {
     if (mode == MODE_DEEP) {
         switch (cls) {
             case 0: case 1: case 2: case 3: launch_sim_t<32, 1, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
