@@ -14,8 +14,10 @@ both arms -- and the denominator the sweep time.
 The default workload is C3 (BASELINE.json configs[2], the north-star config:
 3-model Llama 8B->70B->405B cascade, 1M-request bursty trace, 64-GPU pool).
 
-N>1 runs under torchrun: every rank routes redundantly, the cost-model work is
-sharded over ranks and merged with one NCCL all-gather (strong scaling).
+N>1 runs under torchrun: every rank routes redundantly, the plan chunks are
+dealt round-robin over the ranks, which exchange their p95 bounds after the
+pilot pass and every filter wave and merge with one all-gather -- NCCL calls
+made by the engine library itself on its stream (strong scaling).
 
 --impl reference times the reference CPU planner (oracle/_ref, compiled from
 the unmodified reference sources) on a bounded sample of the same workload and
@@ -224,12 +226,6 @@ def committed_k1_traffic():
         return None
 
 
-class _DevPtr:
-    def __init__(self, ptr, nbytes):
-        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
-                                         "version": 3}
-
-
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -245,12 +241,11 @@ def run_ours(args):
     trace, cfg, N = build_workload(args.config)
     E = eng.Engine(local)
     if world > 1:
-        def allgather(send, recv, nbytes):
-            s = torch.as_tensor(_DevPtr(send, nbytes), device="cuda")
-            r = torch.as_tensor(_DevPtr(recv, nbytes * world), device="cuda")
-            dist.all_gather_into_tensor(r, s)
-            torch.cuda.synchronize()
-        E.set_collective(rank, world, allgather)
+        # the sweep's collectives run inside the engine library on its own
+        # NCCL communicator; torch.distributed only ships the unique id
+        box = [eng.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        E.set_nccl(box[0], rank, world)
     stream = torch.cuda.ExternalStream(E.stream_handle())
 
     # HBM-resident trace (value) and pinned host trace (e2e)
@@ -336,7 +331,9 @@ def run_ours(args):
             "config": dict(config_keys(args.config, trace, N, {"candidates": st_dev[-1]["candidates"],
                                                                 "unique_rows": st_dev[-1]["unique_rows"],
                                                                 "plans": plans}),
-                           parallelism=f"rows sharded over {world} GPU(s), 1 all-gather"),
+                           parallelism=(f"plan chunks dealt round-robin over {world} GPU(s); bound all-gather after the "
+                                        "pilot and every wave, one merge all-gather (NCCL inside the engine library)"
+                                        if world > 1 else "1 GPU")),
             "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": ms_e2e / args.steps,
                     "h2d_bytes_per_step": st_e2e[-1]["h2d_bytes"], "d2h_bytes_per_step": st_e2e[-1]["d2h_bytes"]},
             "gpu_launches": int(sum(s["gpu_launches"] for s in st_dev) + sum(s["gpu_launches"] for s in st_e2e)),

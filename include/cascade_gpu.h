@@ -171,6 +171,7 @@ typedef struct cg_sweep_stats {
     double ms_k1;                 /* the routing/aggregation pass alone */
     double k1_bytes;              /* algorithmic bytes moved by that pass */
     double ms_k4;                 /* the queueing-simulation kernels alone */
+    int64_t collectives;          /* bound exchanges (all-gathers) of a sharded call, final merge excluded */
 } cg_sweep_stats;
 
 /* cascade::outerplan::SweepResult (outerplan.hpp:73-80), flattened. */
@@ -215,6 +216,27 @@ void cg_engine_destroy(cg_engine* engine);
 /* Shard the cost-model work over `world` ranks (this engine is `rank`). */
 cg_status cg_engine_set_collective(cg_engine* engine, int32_t rank, int32_t world,
                                    cg_allgather_fn allgather, void* user);
+/* Multi-GPU inside the library (the CASCADE_PLANNER_THREADS
+ * analogue of util.cpp:31-38).  Sharded calls -- cg_sweep and cg_stage_row --
+ * split every row's plan chunks over the ranks (chunk g -> rank g mod world),
+ * exchange their p95 bounds after the pilot pass and after every filter wave,
+ * and merge the per-budget bests with one all-gather; the result is the
+ * single-GPU result bit for bit.  NCCL is bound at first use (dlopen of
+ * libnccl.so.2, or CG_NCCL_LIBRARY); no torch dependency.
+ *
+ * One process, several GPUs: one member engine per device, one NCCL clique
+ * (ncclCommInitAll), one host thread per device inside each sharded call;
+ * every other call runs on devices[0].  devices = NULL with ndev = 0 takes every
+ * visible device.  cg_engine_destroy releases it all. */
+cg_status cg_engine_create_multi(const int32_t* devices, int32_t ndev, cg_engine** out);
+int32_t cg_engine_device_count(cg_engine* engine);
+/* One process per GPU: rank 0 makes the unique id (cg_nccl_unique_id_bytes()
+ * bytes), the caller's launcher broadcasts it, every rank joins.  Replaces a
+ * cg_engine_set_collective callback; the all-gathers then run in the library
+ * on the engine's stream. */
+int32_t cg_nccl_unique_id_bytes(void);
+cg_status cg_nccl_unique_id(void* out, int32_t capacity);
+cg_status cg_engine_set_nccl(cg_engine* engine, const void* unique_id, int32_t rank, int32_t world);
 /* The engine's CUDA stream (cudaStream_t): every kernel and copy of a call runs
  * on it, so callers can bracket calls with their own CUDA events. */
 void* cg_engine_stream(cg_engine* engine);
@@ -296,8 +318,18 @@ void cg_row_result_free(cg_row_result* result);
 cg_status cg_merge_row_shards(const cg_model* model, const cg_hardware* hw, const cg_cost_params* params,
                               int32_t max_budget, int32_t shards, const uint64_t* lat_bits,
                               const uint64_t* plan_index, cg_row_result** out);
-/* Static contiguous split of `total` work items for `rank` of `world`. */
-void cg_shard_range(uint64_t total, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi);
+/* The plan-index ranges [lo, hi) of row `row` that `rank` of `world`
+ * evaluates in a sharded call whose work list holds rows with num_plans[0..nrows)
+ * plans (rows with 0 plans take no chunks): 64-plan chunks, global chunk g ->
+ * rank g mod world (the device filter's mapping).  Writes up to `cap` pairs,
+ * ascending; returns the number of ranges (-1 on invalid arguments). */
+int64_t cg_shard_row_plans(const uint64_t* num_plans, int32_t nrows, int32_t row, int32_t rank, int32_t world,
+                           uint64_t* ranges, int64_t cap);
+/* Host-only: per-budget best over `shards` partial results with the merge rule
+ * alone (no prefix minimum) -- what one rank holds after its own plans. */
+cg_status cg_merge_budget_bests(const cg_model* model, const cg_hardware* hw, const cg_cost_params* params,
+                                int32_t max_budget, int32_t shards, const uint64_t* lat_bits,
+                                const uint64_t* plan_index, uint64_t* lat_out, uint64_t* plan_out);
 
 /* solve_min_max on a latency table entries[i*(gpu_budget+1) + f]
  * (INFINITY = masked cell).  Writes allocations[stages], per_stage[stages]

@@ -2,6 +2,8 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <sstream>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -21,9 +23,25 @@ cg_engine* engine() {
     static std::once_flag once;
     static std::string error;
     std::call_once(once, [] {
-        int dev = 0;
-        if (const char* s = std::getenv("CASCADE_PLANNER_GPU")) dev = std::atoi(s);
-        cg_status st = cg_engine_create(dev, &holder.e);
+        // CASCADE_PLANNER_GPUS: "all" or a comma-separated device list -> one
+        // engine over those GPUs (sharded sweeps, NCCL inside the library);
+        // otherwise CASCADE_PLANNER_GPU (default 0) alone.
+        cg_status st;
+        const char* multi = std::getenv("CASCADE_PLANNER_GPUS");
+        if (multi && *multi) {
+            std::vector<int32_t> devs;
+            if (std::string(multi) != "all") {  // "all": empty list = every visible device
+                std::stringstream ss(multi);
+                std::string item;
+                while (std::getline(ss, item, ',')) devs.push_back(std::atoi(item.c_str()));
+            }
+            st = cg_engine_create_multi(devs.empty() ? nullptr : devs.data(), static_cast<int32_t>(devs.size()),
+                                        &holder.e);
+        } else {
+            int dev = 0;
+            if (const char* s = std::getenv("CASCADE_PLANNER_GPU")) dev = std::atoi(s);
+            st = cg_engine_create(dev, &holder.e);
+        }
         if (st.code != CG_OK) error = st.message;
     });
     if (!holder.e) throw std::runtime_error("cascade GPU engine unavailable: " + error);

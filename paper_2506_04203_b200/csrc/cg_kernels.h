@@ -184,6 +184,7 @@ struct FilterArgs {
     const unsigned long long* chunk_prefix;    // [nrows+1] cumulative chunk counts per row
     unsigned long long chunk_base;             // first chunk of this launch (waves / rank shard)
     unsigned long long nchunks;                // chunks in this launch
+    int shard_rank, shard_world;               // local chunk l is global chunk l*world + rank (0, 1: unsharded)
     int chunk;                                 // plans per chunk
     const RowDesc* rows;
     const PlanSpace* spaces;

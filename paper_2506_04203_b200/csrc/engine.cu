@@ -12,8 +12,14 @@
 //   -> utopia check -> K6 min-max solve per tuple -> grid-order expansion
 //   -> K7 Tchebycheff argmin per weight, Pareto front -> SweepResult.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <future>
+#include <mutex>
+#include <thread>
 #include <array>
 #include <chrono>
 #include <cmath>
@@ -123,6 +129,21 @@ __global__ void k_accept_stage(const double* __restrict__ scores, long long n, i
     out[r] = acc + 1;
 }
 
+// Bound exchange: ub = min over the gathered ranks' bounds (bit patterns of
+// non-negative doubles order like the values).
+__global__ void k_min_ranks(const unsigned long long* __restrict__ gathered, int world, long long cells,
+                            unsigned long long* __restrict__ ub) {
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    unsigned long long m = gathered[c];
+    for (int r = 1; r < world; ++r) m = min(m, gathered[(long long)r * cells + c]);
+    ub[c] = m;
+}
+
+unsigned long long shard_count(unsigned long long total, int rank, int world) {
+    return total > (unsigned long long)rank ? (total - rank + world - 1) / world : 0ull;
+}
+
 // Cross-rank merge of per-budget bests: minimum latency; equal latency ->
 // parts-lexicographic minimum plan (the reference's `better`, costmodel.cpp:347-352).
 // Gathered layout: rank r occupies [r*2*cells, (r+1)*2*cells): lat bits, then plan.
@@ -159,6 +180,12 @@ struct cg_engine {
     int rank = 0, world = 1;
     cg_allgather_fn allgather = nullptr;
     void* ag_user = nullptr;
+    // NCCL member (cg_engine_create_multi / cg_engine_set_nccl): the sharded
+    // path runs even at world 1, so one device exercises the collective
+    bool nccl_member = false;
+    void* nccl_comm = nullptr;   // ncclComm_t owned by this engine
+    struct MultiGroup* group = nullptr;  // a multi-device engine: its per-device members
+    bool collective() const { return allgather && (world > 1 || nccl_member); }
     int prune = 1;
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
@@ -191,6 +218,19 @@ struct cg_engine {
     SimRunBuffers simbuf;
     DriftBuffers driftbuf;
 };
+
+// A multi-device engine (cg_engine_create_multi): one member engine per
+// device, rank r = members[r], each holding its communicator of one NCCL
+// clique.  Sharded calls (cg_sweep, cg_stage_row) run every member on its
+// own host thread; the rest go to members[0].
+struct MultiGroup {
+    std::vector<cg_engine*> members;
+    std::atomic<bool> broken{false};  // a member failed inside a collective: communicators aborted
+};
+
+namespace {
+cg_engine* primary(cg_engine* e) { return e && e->group ? e->group->members[0] : e; }
+}  // namespace
 
 namespace {
 
@@ -501,7 +541,23 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     // With the pilot pass on, the seeds run in the pilot launch instead.
     std::vector<unsigned long long> seeds;
     const bool use_pilot = E.pilot && E.prune && !prow.empty();
-    if (E.prune && E.world == 1) {
+    const bool collective = E.collective();
+    // Ranks share their bounds: one all-gather of ub and a min over ranks
+    // (every rank's ub is realised by one of its own plans, so the min is a
+    // valid bound for all of them), after the pilot pass and after every wave.
+    auto exchange_ub = [&]() {
+        if (!collective) return;
+        CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
+        x.sync();
+        unsigned long long* gathered = E.d_gather.as<unsigned long long>((size_t)cells * E.world);
+        if (E.allgather(ub, gathered, (size_t)cells * 8, E.ag_user) != 0) fail(CG_ERR_CUDA, "all-gather callback failed");
+        k_min_ranks<<<(unsigned)((cells + 255) / 256), 256, 0, x.s>>>(gathered, E.world, cells, ub);
+        CG_LAUNCH_CHECK();
+        ++x.launches;
+        ++x.st.collectives;
+    };
+    if (E.prune) {
+        int seed_no = 0;
         for (int r = 0; r < nrows; ++r) {
             const auto& sp = hs[rows[r].space];
             if (sp.num_plans < 4096 || N < 1) continue;
@@ -510,7 +566,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                 for (int c = 1; c * sp.shapes[sidx].gpus <= N && c <= 32; ++c) {
                     unsigned long long q = 0;  // lexicographic rank of (0..0, c, 0..0)
                     for (int k = 0; k < c; ++k) q += sp.w(sidx + 1, N - k * sp.shapes[sidx].gpus);
-                    seeds.push_back(((unsigned long long)r << kItemPlanBits) | (q - 1));
+                    if (seed_no++ % E.world == E.rank)  // seeds are dealt round-robin over the ranks
+                        seeds.push_back(((unsigned long long)r << kItemPlanBits) | (q - 1));
                 }
         }
         if (!seeds.empty() && !use_pilot) {
@@ -526,12 +583,15 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned long long* cpre = E.d_iprefix.as<unsigned long long>(chunk_prefix.size());
         x.h2d(rowids, prow.data(), prow.size() * sizeof(int));
         x.h2d(cpre, chunk_prefix.data(), chunk_prefix.size() * 8);
-        uint64_t c_lo = 0, c_hi = 0;
-        cg_shard_range(chunk_prefix.back(), E.rank, E.world, &c_lo, &c_hi);
+        // this rank's chunks: global chunk g belongs to rank g mod world
+        // (local chunk l = global l*world + rank); every rank runs the same
+        // number of waves (the largest share's), so the per-wave bound
+        // exchanges pair up
+        const unsigned long long my_chunks = shard_count(chunk_prefix.back(), E.rank, E.world);
+        const unsigned long long max_chunks = shard_count(chunk_prefix.back(), 0, E.world);
         // list capacity: one wave, but never more than this rank's plans
-        const unsigned long long wave_chunks =
-            std::max<unsigned long long>(1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk,
-                                                                         c_hi - c_lo));
+        const unsigned long long wave_chunks = std::max<unsigned long long>(
+            1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk, max_chunks));
         const unsigned long long cap = wave_chunks * chunk;
         ItemRec* lrecs = E.d_lrecs.as<ItemRec>((size_t)7 * cap);
         unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cap);
@@ -564,8 +624,10 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fp.nrows = (int)prow.size();
             fp.row_ids = rowids;
             fp.chunk_prefix = cpre;
-            fp.chunk_base = c_lo;
-            fp.nchunks = c_hi - c_lo;
+            fp.chunk_base = 0;
+            fp.nchunks = my_chunks;
+            fp.shard_rank = E.rank;
+            fp.shard_world = E.world;
             fp.chunk = chunk;
             fp.rows = base.rows;
             fp.spaces = base.spaces;
@@ -623,9 +685,13 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                 run_list(plists + (size_t)c * pregion, nullptr, pcounts[c], c, true, pperm[c]);
             CG_CUDA(cudaEventRecord(E.ev[11], E.s2));
             pilot_join = true;  // joined before the first bulk list: it overlaps the wave filter
+            if (collective) {
+                exchange_ub();
+                pilot_join = false;
+            }
         }
-        for (unsigned long long w0 = c_lo; w0 < c_hi; w0 += wave_chunks) {
-            const unsigned long long nch = std::min<unsigned long long>(wave_chunks, c_hi - w0);
+        for (unsigned long long w0 = 0; w0 < max_chunks; w0 += wave_chunks) {
+            const unsigned long long nch = w0 < my_chunks ? std::min<unsigned long long>(wave_chunks, my_chunks - w0) : 0;
             CG_CUDA(cudaMemsetAsync(lcount, 0, 7 * 8, x.s));
             FilterArgs fa{};
             fa.N = N;
@@ -637,6 +703,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fa.chunk_prefix = cpre;
             fa.chunk_base = w0;
             fa.nchunks = nch;
+            fa.shard_rank = E.rank;
+            fa.shard_world = E.world;
             fa.chunk = chunk;
             fa.rows = base.rows;
             fa.spaces = base.spaces;
@@ -714,6 +782,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                     CG_CUDA(cudaEventRecord(E.ev[12 + k], streams[k]));
                     CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[12 + k], 0));
                 }
+            if (E.prune && w0 + wave_chunks < max_chunks) exchange_ub();
         }
     }
     CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));  // the pilot's second stream (no-op if unused)
@@ -748,7 +817,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     ra.best_plan = best;
     ra.final_lat = E.d_flat.as<double>(cells);
     ra.final_plan = E.d_fplan.as<long long>(cells);
-    if (E.world > 1) {
+    if (collective) {
         // resolve ties locally, exchange (lat_min, best) with one all-gather, merge
         ResolveArgs local = ra;
         local.nrows = 0;
@@ -1119,12 +1188,178 @@ void free_result(cg_sweep_result* r) {
 // ---------------------------------------------------------------------------
 // C ABI
 
+// ---------------------------------------------------------------------------
+// NCCL inside the library.  libnccl is bound at first use (dlopen), so the
+// library carries no link-time NCCL dependency and, inside a process that
+// already loaded NCCL (e.g. torch's), reuses that copy instead of mapping a
+// second one.  CG_NCCL_LIBRARY overrides the soname.
+namespace {
+struct NcclApi {
+    bool ok = false;
+    std::string error;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GetVersion)(int*) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* env = std::getenv("CG_NCCL_LIBRARY");
+        const char* name = env && *env ? env : "libnccl.so.2";
+        void* h = dlopen(name, RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            api.error = std::string("cannot load NCCL (") + name + "): " + (e ? e : "unknown error");
+            return;
+        }
+        auto sym = [&](auto& fn, const char* n) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, n));
+            if (!fn && api.error.empty()) api.error = std::string("NCCL symbol missing: ") + n;
+        };
+        sym(api.GetUniqueId, "ncclGetUniqueId");
+        sym(api.CommInitRank, "ncclCommInitRank");
+        sym(api.CommInitAll, "ncclCommInitAll");
+        sym(api.AllGather, "ncclAllGather");
+        sym(api.CommDestroy, "ncclCommDestroy");
+        sym(api.CommAbort, "ncclCommAbort");
+        sym(api.GetErrorString, "ncclGetErrorString");
+        sym(api.GetVersion, "ncclGetVersion");
+        api.ok = api.error.empty();
+    });
+    return api;
+}
+
+const NcclApi& nccl_checked() {
+    const NcclApi& n = nccl();
+    if (!n.ok) fail(CG_ERR_CUDA, n.error);
+    return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(CG_ERR_CUDA, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+// The engine's all-gather over its own communicator, enqueued on its stream
+// (the kernels that consume the gathered buffer follow on the same stream).
+int nccl_allgather(const void* send, void* recv, size_t bytes, void* user) {
+    auto* e = static_cast<cg_engine*>(user);
+    const NcclApi& n = nccl();
+    if (!n.ok || !e->nccl_comm) return 1;
+    return n.AllGather(send, recv, bytes, ncclUint8, static_cast<ncclComm_t>(e->nccl_comm), e->s) == ncclSuccess
+               ? 0 : 1;
+}
+
+void join_nccl(cg_engine* e, ncclComm_t comm, int rank, int world) {
+    e->rank = rank;
+    e->world = world;
+    e->allgather = nccl_allgather;
+    e->ag_user = e;
+    e->nccl_member = true;
+    e->nccl_comm = comm;
+}
+
+void release_nccl(cg_engine* e, bool abort) {
+    if (!e->nccl_comm) return;
+    const NcclApi& n = nccl();
+    if (n.ok) (abort ? n.CommAbort : n.CommDestroy)(static_cast<ncclComm_t>(e->nccl_comm));
+    e->nccl_comm = nullptr;
+    e->nccl_member = false;
+    e->allgather = nullptr;
+    e->rank = 0;
+    e->world = 1;
+}
+
+// Runs `call(member, &result)` on every member of a multi-device engine, one
+// host thread per device, and returns rank 0's result.  Counters that are
+// per-rank shares are summed; device times are the maximum over ranks.  A
+// member that fails while the others are still running (they may be waiting
+// in a collective) aborts every communicator after a grace period, so no
+// call can hang; the group then refuses further sharded calls.
+template <class R, class Call, class Free>
+cg_status run_group(cg_engine* E, R** out, Call&& call, Free&& free_fn) {
+    MultiGroup& g = *E->group;
+    if (g.broken) return err_status(CG_ERR_CUDA, "multi-device engine unusable: its NCCL communicators were aborted");
+    const int n = (int)g.members.size();
+    std::vector<R*> res(n, nullptr);
+    std::vector<cg_status> st(n);
+    std::vector<std::future<void>> fut;
+    for (int r = 0; r < n; ++r)
+        fut.push_back(std::async(std::launch::async, [&, r] { st[r] = call(g.members[r], &res[r]); }));
+    bool failed_early = false;
+    for (;;) {
+        int done = 0, failed = 0;
+        for (int r = 0; r < n; ++r)
+            if (fut[r].wait_for(std::chrono::milliseconds(0)) == std::future_status::ready) {
+                ++done;
+                failed += st[r].code != CG_OK;
+            }
+        if (done == n) break;
+        if (failed && !failed_early) {
+            failed_early = true;
+            // deterministic errors (validation) reach every rank within
+            // moments; a lone failure leaves the others in a collective
+            bool all_done = false;
+            for (int t = 0; t < 200 && !all_done; ++t) {
+                std::this_thread::sleep_for(std::chrono::milliseconds(50));
+                all_done = true;
+                for (int r = 0; r < n; ++r)
+                    all_done &= fut[r].wait_for(std::chrono::milliseconds(0)) == std::future_status::ready;
+            }
+            if (!all_done) {
+                g.broken = true;
+                for (cg_engine* m : g.members)
+                    if (m->nccl_comm) nccl().CommAbort(static_cast<ncclComm_t>(m->nccl_comm));
+            }
+            continue;
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    if (g.broken)
+        for (cg_engine* m : g.members) m->nccl_comm = nullptr;  // aborted above
+    for (int r = 0; r < n; ++r)
+        if (st[r].code != CG_OK) {
+            for (R* p : res)
+                if (p) free_fn(p);
+            return st[r];
+        }
+    cg_sweep_stats& s0 = res[0]->stats;
+    for (int r = 1; r < n; ++r) {
+        const cg_sweep_stats& s = res[r]->stats;
+        s0.plans_stable += s.plans_stable;
+        s0.plans_simulated_full += s.plans_simulated_full;
+        s0.plans_pruned += s.plans_pruned;
+        s0.plans_bound_skipped += s.plans_bound_skipped;
+        s0.plans_seeded += s.plans_seeded;
+        s0.plans_overflow += s.plans_overflow;
+        s0.request_steps += s.request_steps;
+        s0.h2d_bytes += s.h2d_bytes;
+        s0.d2h_bytes += s.d2h_bytes;
+        s0.gpu_launches += s.gpu_launches;
+        s0.ms_rows = std::max(s0.ms_rows, s.ms_rows);
+        s0.ms_k4 = std::max(s0.ms_k4, s.ms_k4);
+        s0.ms_total = std::max(s0.ms_total, s.ms_total);
+        free_fn(res[r]);
+    }
+    *out = res[0];
+    return ok_status();
+}
+}  // namespace
+
 extern "C" {
 
 const char* cg_version(void) { return "cascade-gpu 0.1 (sm_100a)"; }
 
 cg_status cg_sweep_result_json(cg_engine* E, const cg_sweep_result* r, int32_t indent, int32_t what,
                                int32_t flags, char** text, int64_t* len) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !r || !text || !len) fail(CG_ERR_INVALID_INPUT, "null engine/result/output");
         if (indent < 0) fail(CG_ERR_UNSUPPORTED, "compact JSON (indent < 0) is not produced by the planner");
@@ -1172,6 +1407,7 @@ static double host_at(cg_engine* E, const cg_trace* tr, const double* col, long 
 
 cg_status cg_drift_windows(cg_engine* E, const cg_trace* tr, const cg_drift_stats* base, const cg_drift_policy* pol,
                            cg_drift_result** out) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !tr || !base || !pol || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
         *out = nullptr;
@@ -1229,6 +1465,7 @@ void cg_drift_result_free(cg_drift_result* r) {
 }
 
 cg_status cg_trace_baseline(cg_engine* E, const cg_trace* tr, int32_t has_h1, double h1, cg_drift_stats* out) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !tr || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
         *out = cg_drift_stats{0, 0, 0, 1, has_h1, h1};
@@ -1267,6 +1504,7 @@ void cg_sim_result_free(cg_sim_result* r) {
 cg_status cg_simulate(cg_engine* E, const cg_trace* tr, const cg_model* models, int32_t C, const cg_hardware* hw,
                       const cg_cost_params* q, const cg_sim_config* cfg, const cg_cascade_plan* plans,
                       int32_t P, int32_t compare, cg_sim_result** out) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !tr || !models || !hw || !q || !cfg || (P > 0 && !plans) || !out)
             fail(CG_ERR_INVALID_INPUT, "null argument");
@@ -1473,10 +1711,12 @@ static cg_status ingest_common(cg_engine* E, const char* bytes, int64_t len, con
 
 cg_status cg_parse_trace_jsonl(cg_engine* E, const char* bytes, int64_t len, const char* path,
                                cg_trace_buffer** out) {
+    E = primary(E);
     return ingest_common(E, bytes, len, path ? path : "<memory>", 0.0, out);
 }
 
 cg_status cg_read_trace_jsonl(cg_engine* E, const char* path, cg_trace_buffer** out) {
+    E = primary(E);
     if (!E || !path || !out) return err_status(CG_ERR_INVALID_INPUT, "null engine/path");
     Timer tm;
     FILE* f = std::fopen(path, "rb");
@@ -1520,11 +1760,21 @@ cg_status cg_engine_create(int32_t device, cg_engine** out) {
     });
 }
 
-void* cg_engine_stream(cg_engine* e) { return e ? static_cast<void*>(e->s) : nullptr; }
+void* cg_engine_stream(cg_engine* e) {
+    e = primary(e);
+    return e ? static_cast<void*>(e->s) : nullptr;
+}
 
 void cg_engine_destroy(cg_engine* e) {
     if (!e) return;
+    if (e->group) {
+        for (cg_engine* m : e->group->members) cg_engine_destroy(m);
+        delete e->group;
+        delete e;
+        return;
+    }
     cudaSetDevice(e->device);
+    release_nccl(e, false);
     for (auto& ev : e->ev) cudaEventDestroy(ev);
     if (e->s) cudaStreamDestroy(e->s);
     if (e->s2) cudaStreamDestroy(e->s2);
@@ -1536,6 +1786,7 @@ void cg_engine_destroy(cg_engine* e) {
 cg_status cg_engine_set_collective(cg_engine* e, int32_t rank, int32_t world, cg_allgather_fn fn, void* user) {
     return guarded([&] {
         if (!e) fail(CG_ERR_INVALID_INPUT, "null engine");
+        if (e->group || e->nccl_member) fail(CG_ERR_INVALID_INPUT, "engine already bound to NCCL communicators");
         if (world < 1 || rank < 0 || rank >= world) fail(CG_ERR_INVALID_INPUT, "invalid rank/world");
         if (world > 1 && !fn) fail(CG_ERR_INVALID_INPUT, "multi-rank engine needs an all-gather callback");
         e->rank = rank;
@@ -1545,9 +1796,88 @@ cg_status cg_engine_set_collective(cg_engine* e, int32_t rank, int32_t world, cg
     });
 }
 
+cg_status cg_nccl_unique_id(void* out, int32_t capacity) {
+    return guarded([&] {
+        if (!out || capacity < (int32_t)sizeof(ncclUniqueId)) fail(CG_ERR_INVALID_INPUT, "unique id buffer too small");
+        ncclUniqueId id;
+        nccl_check(nccl_checked().GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, &id, sizeof(id));
+    });
+}
+
+int32_t cg_nccl_unique_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+cg_status cg_engine_set_nccl(cg_engine* e, const void* unique_id, int32_t rank, int32_t world) {
+    return guarded([&] {
+        if (!e || !unique_id) fail(CG_ERR_INVALID_INPUT, "null engine/unique id");
+        if (e->group) fail(CG_ERR_INVALID_INPUT, "a multi-device engine already owns its communicators");
+        if (world < 1 || rank < 0 || rank >= world) fail(CG_ERR_INVALID_INPUT, "invalid rank/world");
+        const NcclApi& n = nccl_checked();
+        CG_CUDA(cudaSetDevice(e->device));
+        release_nccl(e, false);
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof(id));
+        ncclComm_t comm = nullptr;
+        nccl_check(n.CommInitRank(&comm, world, id, rank), "ncclCommInitRank");
+        join_nccl(e, comm, rank, world);
+    });
+}
+
+cg_status cg_engine_create_multi(const int32_t* devices, int32_t ndev, cg_engine** out) {
+    std::vector<cg_engine*> made;
+    cg_status st = guarded([&] {
+        if (!out) fail(CG_ERR_INVALID_INPUT, "null output");
+        *out = nullptr;
+        std::vector<int32_t> all;
+        if (!devices && ndev == 0) {  // every visible device
+            int n = 0;
+            if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+                fail(CG_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+            for (int i = 0; i < n; ++i) all.push_back(i);
+            devices = all.data();
+            ndev = n;
+        }
+        if (!devices || ndev < 1) fail(CG_ERR_INVALID_INPUT, "multi-device engine needs at least one device");
+        for (int i = 0; i < ndev; ++i)
+            for (int j = 0; j < i; ++j)
+                if (devices[i] == devices[j]) fail(CG_ERR_INVALID_INPUT, "duplicate device in the multi-device engine");
+        const NcclApi& n = nccl_checked();
+        for (int i = 0; i < ndev; ++i) {
+            cg_engine* m = nullptr;
+            cg_status cs = cg_engine_create(devices[i], &m);
+            if (cs.code != CG_OK) fail(cs.code, cs.message);
+            made.push_back(m);
+        }
+        std::vector<ncclComm_t> comms(ndev, nullptr);
+        nccl_check(n.CommInitAll(comms.data(), ndev, devices), "ncclCommInitAll");
+        for (int i = 0; i < ndev; ++i) join_nccl(made[i], comms[i], i, ndev);
+        auto* parent = new cg_engine();
+        parent->device = devices[0];
+        parent->sm_count = made[0]->sm_count;
+        parent->group = new MultiGroup();
+        parent->group->members = made;
+        *out = parent;
+    });
+    if (st.code != CG_OK)
+        for (cg_engine* m : made) cg_engine_destroy(m);
+    return st;
+}
+
+int32_t cg_engine_device_count(cg_engine* e) {
+    if (!e) return 0;
+    return e->group ? (int32_t)e->group->members.size() : 1;
+}
+
 cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
     return guarded([&] {
         if (!e || !key) fail(CG_ERR_INVALID_INPUT, "null engine/key");
+        if (e->group) {
+            for (cg_engine* m : e->group->members) {
+                cg_status ms = cg_engine_set_option(m, key, value);
+                if (ms.code != CG_OK) fail(ms.code, ms.message);
+            }
+            return;
+        }
         const std::string k(key);
         if (k == "prune") e->prune = value ? 1 : 0;
         else if (k == "k1_form") e->k1_form = (int)value;
@@ -1572,6 +1902,12 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
 cg_status cg_sweep(cg_engine* E, const cg_trace* tr, const cg_model* models, int32_t C, const cg_hardware* hw,
                    const cg_cost_params* q, int32_t total_gpus, const cg_sweep_config* cfg,
                    cg_sweep_result** out) {
+    if (E && E->group) {
+        if (!out) return err_status(CG_ERR_INVALID_INPUT, "null argument");
+        return run_group(E, out, [&](cg_engine* m, cg_sweep_result** o) {
+            return cg_sweep(m, tr, models, C, hw, q, total_gpus, cfg, o);
+        }, cg_sweep_result_free);
+    }
     return guarded([&] {
         Timer timer;
         if (out) *out = nullptr;
@@ -1878,6 +2214,7 @@ void cg_sweep_result_free(cg_sweep_result* r) { free_result(r); }
 
 cg_status cg_route(cg_engine* E, const cg_trace* tr, const double* thresholds, const int32_t* deployed,
                    cg_route_result* out, int32_t* accept_stage) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !tr || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
         CG_CUDA(cudaSetDevice(E->device));
@@ -1945,6 +2282,7 @@ cg_status cg_route(cg_engine* E, const cg_trace* tr, const double* thresholds, c
 }
 
 cg_status cg_route_grid(cg_engine* E, const cg_trace* tr, const cg_sweep_config* cfg, cg_route_grid_result** out) {
+    E = primary(E);
     return guarded([&] {
         Timer timer;
         if (out) *out = nullptr;
@@ -2103,15 +2441,78 @@ cg_status cg_merge_row_shards(const cg_model* model, const cg_hardware* hw, cons
     });
 }
 
-/* Item range [lo, hi) of `rank` among `world` for a list of `total` items (the
- * static contiguous split used by every sharded kernel class). */
-void cg_shard_range(uint64_t total, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi) {
-    *lo = total * (uint64_t)rank / (uint64_t)world;
-    *hi = total * (uint64_t)(rank + 1) / (uint64_t)world;
+/* Plan ranges a rank evaluates: the host restatement of k_plan_filter's chunk
+ * mapping (shard_global_chunk, shared with the kernel) over the same chunk
+ * list evaluate_rows builds (rows with plans, 64-plan chunks, reversed). */
+int64_t cg_shard_row_plans(const uint64_t* num_plans, int32_t nrows, int32_t row, int32_t rank, int32_t world,
+                           uint64_t* ranges, int64_t cap) {
+    if (!num_plans || nrows < 1 || row < 0 || row >= nrows || world < 1 || rank < 0 || rank >= world) return -1;
+    const unsigned long long chunk = 64;
+    unsigned long long first = 0;  // chunk_prefix of `row`
+    for (int r = 0; r < row; ++r) first += (num_plans[r] + chunk - 1) / chunk;
+    const unsigned long long P = num_plans[row], nrc = (P + chunk - 1) / chunk;
+    unsigned long long total = first + nrc;
+    for (int r = row + 1; r < nrows; ++r) total += (num_plans[r] + chunk - 1) / chunk;
+    const unsigned long long mine = shard_count(total, rank, world);
+    std::vector<std::pair<unsigned long long, unsigned long long>> out;
+    // local chunks whose global chunk lies in [first, first + nrc)
+    unsigned long long l0 = first > (unsigned long long)rank ? (first - rank + world - 1) / world : 0;
+    for (unsigned long long l = l0; l < mine; ++l) {
+        const unsigned long long g = shard_global_chunk(l, rank, world);
+        if (g >= first + nrc) break;
+        const unsigned long long j = nrc - 1 - (g - first);
+        out.emplace_back(j * chunk, std::min(j * chunk + chunk, P));
+    }
+    std::sort(out.begin(), out.end());
+    for (size_t i = 0; i < out.size() && (int64_t)i < cap; ++i) {
+        ranges[2 * i] = out[i].first;
+        ranges[2 * i + 1] = out[i].second;
+    }
+    return (int64_t)out.size();
+}
+
+/* Per-budget reduction of shard bests with merge_take (the rule of the
+ * device's atomicMin + tie resolve and of k_merge_ranks), no prefix minimum. */
+cg_status cg_merge_budget_bests(const cg_model* model, const cg_hardware* hw, const cg_cost_params* q,
+                                int32_t max_budget, int32_t shards, const uint64_t* lat_bits,
+                                const uint64_t* plan_index, uint64_t* lat_out, uint64_t* plan_out) {
+    return guarded([&] {
+        if (!model || !hw || !q || !lat_bits || !plan_index || !lat_out || !plan_out || shards < 1 || max_budget < 0)
+            fail(CG_ERR_INVALID_INPUT, "invalid merge arguments");
+        const int N = max_budget;
+        HostPlanSpace hs;
+        hs.build(legal_shapes(*model, *hw, *q), N);
+        PlanSpace sp;
+        std::memset(&sp, 0, sizeof(sp));
+        sp.S = (int)hs.shapes.size();
+        sp.N = N;
+        for (int k = 0; k < sp.S; ++k) sp.shapes[k] = hs.shapes[k];
+        sp.ways = hs.ways.data();
+        sp.num_plans = hs.num_plans;
+        for (int g = 0; g <= N; ++g) {
+            unsigned long long bl = kInfBits, bp = ~0ull;
+            for (int s = 0; s < shards; ++s) {
+                const unsigned long long l = lat_bits[(size_t)s * (N + 1) + g];
+                const unsigned long long p = plan_index[(size_t)s * (N + 1) + g];
+                if (merge_take(sp, l, p, bl, bp)) {
+                    bl = l;
+                    bp = p;
+                }
+            }
+            lat_out[g] = bl;
+            plan_out[g] = bp;
+        }
+    });
 }
 
 cg_status cg_stage_row(cg_engine* E, const cg_model* model, const cg_workload* w, const cg_hardware* hw,
                        const cg_cost_params* q, int32_t max_budget, cg_row_result** out) {
+    if (E && E->group) {
+        if (!out) return err_status(CG_ERR_INVALID_INPUT, "null argument");
+        return run_group(E, out, [&](cg_engine* m, cg_row_result** o) {
+            return cg_stage_row(m, model, w, hw, q, max_budget, o);
+        }, cg_row_result_free);
+    }
     return guarded([&] {
         if (out) *out = nullptr;
         if (!E || !model || !w || !hw || !q || !out) fail(CG_ERR_INVALID_INPUT, "null argument");
@@ -2187,6 +2588,7 @@ void cg_row_result_free(cg_row_result* r) {
 cg_status cg_solve_min_max(cg_engine* E, const double* entries, int32_t stages, int32_t gpu_budget,
                            int32_t total_gpus, int32_t* allocations, double* per_stage_latency,
                            double* objective_L) {
+    E = primary(E);
     return guarded([&] {
         if (!E || !entries) fail(CG_ERR_INVALID_INPUT, "null argument");
         CG_CUDA(cudaSetDevice(E->device));

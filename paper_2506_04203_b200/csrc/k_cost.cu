@@ -1417,16 +1417,19 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
     int row = 0;
     unsigned long long lo = 0, hi = 0;
     if (active) {
-        int l = 0, h = a.nrows - 1;  // chunk_prefix[l] <= chunk < chunk_prefix[l+1]
+        // this rank's chunks interleave with the other ranks' (chunk g belongs
+        // to rank g mod world): every rank sees every row's plan mix
+        const unsigned long long g = shard_global_chunk(chunk + a.chunk_base, a.shard_rank, a.shard_world);
+        int l = 0, h = a.nrows - 1;  // chunk_prefix[l] <= g < chunk_prefix[l+1]
         while (l < h) {
             const int mid = (l + h + 1) >> 1;
-            if (a.chunk_prefix[mid] <= chunk + a.chunk_base) l = mid;
+            if (a.chunk_prefix[mid] <= g) l = mid;
             else h = mid - 1;
         }
         row = a.row_ids[l];
         // reversed within the row: large-shape plans (best bounds) first
         const unsigned long long nrc = a.chunk_prefix[l + 1] - a.chunk_prefix[l];
-        const unsigned long long j = nrc - 1 - (chunk + a.chunk_base - a.chunk_prefix[l]);
+        const unsigned long long j = nrc - 1 - (g - a.chunk_prefix[l]);
         const unsigned long long P = a.spaces[a.rows[row].space].num_plans;
         lo = j * (unsigned long long)a.chunk;
         hi = lo + a.chunk < P ? lo + a.chunk : P;

@@ -61,6 +61,13 @@ __host__ __device__ inline bool merge_take(const PlanSpace& sp, unsigned long lo
 
 // '<' of CompactPlan::parts (vector<pair<shape, count>>, costmodel.cpp:351)
 // evaluated on dense count vectors.
+// Sharded calls: local work chunk l of `rank` is global chunk l*world + rank
+// of the sweep's chunk list (64 consecutive plan indices per chunk, rows in
+// list order, each row's chunks from its last to its first).
+__host__ __device__ __forceinline__ unsigned long long shard_global_chunk(unsigned long long l, int rank, int world) {
+    return l * (unsigned long long)(world > 0 ? world : 1) + (unsigned long long)rank;
+}
+
 __host__ __device__ inline bool parts_less(const unsigned char* A, const unsigned char* B, int S) {
     for (int s = 0; s < S; ++s) {
         if (A[s] == B[s]) continue;

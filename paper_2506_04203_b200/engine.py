@@ -107,7 +107,7 @@ class SweepStats(ctypes.Structure):
         "plans_stable", "plans_simulated_full", "plans_pruned", "plans_bound_skipped", "plans_seeded", "plans_overflow", "request_steps",
         "h2d_bytes", "d2h_bytes")] + [("num_ranks", ctypes.c_int32), ("gpu_launches", ctypes.c_int32)] + \
         [(n, ctypes.c_double) for n in ("ms_total", "ms_route", "ms_quality", "ms_rows", "ms_solve",
-                                        "ms_k1", "k1_bytes", "ms_k4")]
+                                        "ms_k1", "k1_bytes", "ms_k4")] + [("collectives", ctypes.c_int64)]
 
 
 class SweepResultC(ctypes.Structure):
@@ -259,9 +259,11 @@ ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, 
 EXPORTED = ["cg_engine_create", "cg_engine_destroy", "cg_engine_stream", "cg_engine_set_collective", "cg_engine_set_option",
             "cg_sweep", "cg_sweep_result_free", "cg_route", "cg_stage_row", "cg_row_result_free",
             "cg_solve_min_max", "cg_generate_trace", "cg_version", "cg_route_grid", "cg_route_grid_result_free",
-            "cg_merge_row_shards", "cg_shard_range", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
+            "cg_merge_row_shards", "cg_shard_row_plans", "cg_merge_budget_bests", "cg_read_trace_jsonl", "cg_parse_trace_jsonl",
             "cg_trace_buffer_free", "cg_sweep_result_json", "cg_text_free", "cg_simulate",
-            "cg_sim_result_free", "cg_drift_windows", "cg_drift_result_free", "cg_trace_baseline"]
+            "cg_sim_result_free", "cg_drift_windows", "cg_drift_result_free", "cg_trace_baseline",
+            "cg_engine_create_multi", "cg_engine_device_count", "cg_nccl_unique_id_bytes", "cg_nccl_unique_id",
+            "cg_engine_set_nccl"]
 
 _lib = None
 
@@ -280,6 +282,17 @@ def library():
         L.cg_engine_set_collective.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                                ALLGATHER_FN, ctypes.c_void_p]
         L.cg_engine_set_collective.restype = Status
+        L.cg_engine_create_multi.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                                             ctypes.POINTER(ctypes.c_void_p)]
+        L.cg_engine_create_multi.restype = Status
+        L.cg_engine_device_count.argtypes = [ctypes.c_void_p]
+        L.cg_engine_device_count.restype = ctypes.c_int32
+        L.cg_nccl_unique_id_bytes.argtypes = []
+        L.cg_nccl_unique_id_bytes.restype = ctypes.c_int32
+        L.cg_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        L.cg_nccl_unique_id.restype = Status
+        L.cg_engine_set_nccl.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32]
+        L.cg_engine_set_nccl.restype = Status
         L.cg_engine_set_option.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int64]
         L.cg_engine_set_option.restype = Status
         L.cg_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(Trace), ctypes.POINTER(Model), ctypes.c_int32,
@@ -300,9 +313,14 @@ def library():
                                           ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
                                           ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.POINTER(RowResultC))]
         L.cg_merge_row_shards.restype = Status
-        L.cg_shard_range.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
-                                     ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
-        L.cg_shard_range.restype = None
+        L.cg_shard_row_plans.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
+        L.cg_shard_row_plans.restype = ctypes.c_int64
+        L.cg_merge_budget_bests.argtypes = [ctypes.POINTER(Model), ctypes.POINTER(Hardware), ctypes.POINTER(CostParams),
+                                            ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint64),
+                                            ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                            ctypes.POINTER(ctypes.c_uint64)]
+        L.cg_merge_budget_bests.restype = Status
         L.cg_stage_row.argtypes = [ctypes.c_void_p, ctypes.POINTER(Model), ctypes.POINTER(Workload),
                                    ctypes.POINTER(Hardware), ctypes.POINTER(CostParams), ctypes.c_int32,
                                    ctypes.POINTER(ctypes.POINTER(RowResultC))]
@@ -490,13 +508,28 @@ def _sweep_config_c(cfg: Optional[dict]):
     return c, (sizes, vals)
 
 
-class Engine:
-    """One engine per GPU (cg_engine)."""
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the engine library (rank 0 of a multi-process sweep)."""
+    L = library()
+    n = L.cg_nccl_unique_id_bytes()
+    buf = ctypes.create_string_buffer(n)
+    _check(L.cg_nccl_unique_id(buf, n))
+    return buf.raw
 
-    def __init__(self, device: int = 0):
+
+class Engine:
+    """One engine per GPU (cg_engine), or with `devices` one engine over
+    several GPUs of this process (cg_engine_create_multi: NCCL clique, sharded
+    sweeps)."""
+
+    def __init__(self, device: int = 0, devices: Optional[Sequence[int]] = None):
         self._lib = library()
         h = ctypes.c_void_p()
-        _check(self._lib.cg_engine_create(int(device), ctypes.byref(h)))
+        if devices is not None:
+            arr = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+            _check(self._lib.cg_engine_create_multi(arr, len(devices), ctypes.byref(h)))
+        else:
+            _check(self._lib.cg_engine_create(int(device), ctypes.byref(h)))
         self._h = h
         self._ag_keep = None
         self.last_stats: dict = {}
@@ -518,6 +551,14 @@ class Engine:
 
     def set_option(self, key: str, value: int):
         _check(self._lib.cg_engine_set_option(self._h, key.encode(), int(value)))
+
+    def device_count(self) -> int:
+        return int(self._lib.cg_engine_device_count(self._h))
+
+    def set_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Joins an NCCL communicator (one process per GPU); the library then
+        runs the sweep's all-gathers itself on the engine's stream."""
+        _check(self._lib.cg_engine_set_nccl(self._h, unique_id, int(rank), int(world)))
 
     def set_collective(self, rank: int, world: int, allgather) -> None:
         """allgather(send_ptr, recv_ptr, nbytes) -> None, device pointers."""
@@ -790,11 +831,37 @@ def generate_trace(spec: dict, seed: int) -> dict:
             "scores": sc[: n * c].reshape(c, n)}
 
 
-def shard_range(total: int, rank: int, world: int):
-    """Static contiguous split used by every sharded kernel class."""
-    lo, hi = ctypes.c_uint64(), ctypes.c_uint64()
-    library().cg_shard_range(int(total), int(rank), int(world), ctypes.byref(lo), ctypes.byref(hi))
-    return lo.value, hi.value
+def shard_row_plans(num_plans, row: int, rank: int, world: int):
+    """Plan ranges [(lo, hi), ...] of row `row` that `rank` evaluates in a
+    sharded call over rows with `num_plans` plans (the device filter's chunk
+    mapping, cg_shard_row_plans)."""
+    L = library()
+    U64 = ctypes.POINTER(ctypes.c_uint64)
+    npl = np.ascontiguousarray(num_plans, dtype=np.uint64)
+    n = L.cg_shard_row_plans(npl.ctypes.data_as(U64), len(npl), int(row), int(rank), int(world), None, 0)
+    if n < 0:
+        raise CascadeError(0, "invalid shard arguments")
+    out = np.zeros(max(1, 2 * n), dtype=np.uint64)
+    L.cg_shard_row_plans(npl.ctypes.data_as(U64), len(npl), int(row), int(rank), int(world),
+                         out.ctypes.data_as(U64), n)
+    return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n)]
+
+
+def merge_budget_bests(hw: dict, params: Optional[dict], model: dict, max_budget: int, lat_bits, plan_index):
+    """Per-budget best over partial results (merge rule only, no prefix min)."""
+    L = library()
+    lat = np.ascontiguousarray(lat_bits, dtype=np.uint64).reshape(-1)
+    idx = np.ascontiguousarray(plan_index, dtype=np.uint64).reshape(-1)
+    shards = lat.size // (max_budget + 1)
+    marr, keep = models_c([model])
+    hwc, pc = hardware_c(hw), params_c(params)
+    lo = np.zeros(max_budget + 1, dtype=np.uint64)
+    po = np.zeros(max_budget + 1, dtype=np.uint64)
+    U64 = ctypes.POINTER(ctypes.c_uint64)
+    _check(L.cg_merge_budget_bests(marr, ctypes.byref(hwc), ctypes.byref(pc), int(max_budget), int(shards),
+                                   lat.ctypes.data_as(U64), idx.ctypes.data_as(U64), lo.ctypes.data_as(U64),
+                                   po.ctypes.data_as(U64)))
+    return lo, po
 
 
 def merge_row_shards(hw: dict, params: Optional[dict], model: dict, max_budget: int, lat_bits, plan_index) -> dict:

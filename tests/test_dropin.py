@@ -17,8 +17,11 @@ BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
 
 
 @pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in binary not built (make -C oracle dropin)")
+@pytest.mark.parametrize("gpus", ["", "all"])
 @pytest.mark.parametrize("name", ["fixture2", "three_stage"])
-def test_cli_outputs_byte_identical(tmp_path, name):
+def test_cli_outputs_byte_identical(tmp_path, name, gpus):
+    """gpus="all": CASCADE_PLANNER_GPUS makes the binding create one engine over
+    every visible GPU (cg_engine_create_multi, NCCL inside the library)."""
     if name == "fixture2":
         hw = W.hardware(8)
         hw["gpus_per_node"] = 4
@@ -37,7 +40,8 @@ def test_cli_outputs_byte_identical(tmp_path, name):
     (tmp_path / "config.json").write_text(json.dumps(cfg))
     (tmp_path / "spec.json").write_text(json.dumps(spec))
     r = subprocess.run([BIN, str(tmp_path / "config.json"), str(tmp_path / "spec.json"), "7",
-                        str(tmp_path / "out"), str(minq)], capture_output=True, text=True, timeout=600)
+                        str(tmp_path / "out"), str(minq)], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, CASCADE_PLANNER_GPUS=gpus))
     assert r.returncode == 0, r.stdout + r.stderr
     rep = json.loads(r.stdout.strip().splitlines()[-1])
     assert rep["identical"], rep

@@ -1,12 +1,16 @@
 """CPU multi-process tests of the N>1 path (gloo, world size 2 and 3).
 
-The multi-GPU sweep shards every row's plan-index space with a static
-contiguous split (cg_shard_range), each rank reduces its shard to per-budget
-bests, one all-gather exchanges them and every rank merges with the
-reference's tie-break (merge_take, shared by the device merge kernel and
-cg_merge_row_shards).  Here the shards are evaluated by the C oracle, the
-exchange is a real torch.distributed all-gather over gloo, and the merged
-row must equal the unsharded row bit for bit.
+The multi-GPU sweep deals the 64-plan chunks of its work list (every row's
+plan-index space, rows in list order) round-robin over the ranks
+(cg_shard_row_plans restates the device filter's mapping, shard_global_chunk),
+each rank reduces its chunks to per-budget bests (cg_merge_budget_bests: the
+rule of the device atomicMin + tie resolve), one all-gather exchanges them and
+every rank merges with the reference's tie-break (merge_take, shared by the
+device merge kernel and cg_merge_row_shards).  Here the engine library decides
+which plans each rank owns and performs both merges; the per-chunk bests come
+from the C oracle (no GPU here); the exchange is a real torch.distributed
+all-gather over gloo, and the merged rows must equal the unsharded rows bit
+for bit.
 """
 import math
 import os
@@ -50,11 +54,16 @@ def worker(rank, world, port, results):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        # one work list holding the three rows, in order (chunk offsets matter)
+        totals = [cpy.row_shard(HW, PARAMS, W.model_spec(m, 1), wl, N, 0, 0)[2] for m, wl, N in CASES]
         for ci, (mname, wl, N) in enumerate(CASES):
             model = W.model_spec(mname, 1)
-            _, _, total = cpy.row_shard(HW, PARAMS, model, wl, N, 0, 0)
-            lo, hi = eng.shard_range(total, rank, world)
-            bits, idx, _ = cpy.row_shard(HW, PARAMS, model, wl, N, lo, hi)
+            parts = [cpy.row_shard(HW, PARAMS, model, wl, N, lo, hi)
+                     for lo, hi in eng.shard_row_plans(totals, ci, rank, world)]
+            none = np.full(N + 1, np.iinfo(np.uint64).max, dtype=np.uint64)
+            lat = np.stack([p[0] for p in parts]) if parts else none[None]
+            pid = np.stack([p[1] for p in parts]) if parts else none[None]
+            bits, idx = eng.merge_budget_bests(HW, PARAMS, model, N, lat, pid)
             mine = torch.from_numpy(np.stack([bits.view(np.int64), idx.view(np.int64)]))
             gathered = [torch.empty_like(mine) for _ in range(world)]
             dist.all_gather(gathered, mine)
@@ -79,10 +88,21 @@ def test_sharded_rows_merge_to_the_unsharded_row(world):
             assert not diff_json(got, full), (world, rank, ci, diff_json(got, full)[:3])
 
 
-def test_shard_ranges_partition_the_items():
-    for total in (0, 1, 7, 1000, 490772):
+def test_shard_row_plans_partition_every_row():
+    lists = [[0], [1], [7], [1000], [490772], [64, 0, 65, 129, 3], [5000, 7, 0, 64 * 13]]
+    for num_plans in lists:
+        nchunks = sum((p + 63) // 64 for p in num_plans)
         for world in (1, 2, 3, 8):
-            spans = [eng.shard_range(total, r, world) for r in range(world)]
-            assert spans[0][0] == 0 and spans[-1][1] == total
-            for (a, b), (c, d) in zip(spans, spans[1:]):
-                assert b == c and a <= b
+            owned = [0] * world
+            for row, P in enumerate(num_plans):
+                cover = np.zeros(P, dtype=np.int32)
+                for rank in range(world):
+                    rs = eng.shard_row_plans(num_plans, row, rank, world)
+                    assert rs == sorted(rs)
+                    for lo, hi in rs:
+                        assert 0 <= lo < hi <= P and (hi - lo == 64 or hi == P) and lo % 64 == 0
+                        cover[lo:hi] += 1
+                        owned[rank] += 1
+                assert (cover == 1).all(), (num_plans, row, world)
+            # chunks are dealt round-robin: shares differ by at most one chunk
+            assert sum(owned) == nchunks and max(owned) - min(owned) <= 1
