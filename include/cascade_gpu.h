@@ -172,6 +172,8 @@ typedef struct cg_sweep_stats {
     double k1_bytes;              /* algorithmic bytes moved by that pass */
     double ms_k4;                 /* the queueing-simulation kernels alone */
     int64_t collectives;          /* bound exchanges (all-gathers) of a sharded call, final merge excluded */
+    int64_t quality_blocks;       /* K2 (tuple, request block) pairs */
+    int64_t quality_blocks_seq;   /* of those, folded request by request (binade crossings, ties, s = 0) */
 } cg_sweep_stats;
 
 /* cascade::outerplan::SweepResult (outerplan.hpp:73-80), flattened. */
@@ -253,7 +255,10 @@ void* cg_engine_stream(cg_engine* engine);
  *   "wave_plans"       64 (default) plans per filter wave in units of 2^20 (~248 B of HBM per plan)
  *   "conc_lists_max"   65536 (default) waves with at most this many listed plans run their
  *                      replica-count classes concurrently on four streams (0: never)
- *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle" (diagnostic)
+ *   "quality_form"     1 (default) block-parallel exact K2 quality sums; 0 one fp64 add chain per tuple
+ *   "p95_tables"       1 (default) K3 chunk tables for traces >= 65536 requests; 0 direct column scans
+ *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle",
+ *   "quality_block" (diagnostic)
  * Unknown keys return CG_ERR_INVALID_INPUT. */
 cg_status cg_engine_set_option(cg_engine* engine, const char* key, int64_t value);
 

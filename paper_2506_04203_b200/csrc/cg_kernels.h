@@ -66,13 +66,25 @@ void launch_workload_seq_sums(const WorkloadArgs& a, const unsigned long long* r
 void launch_make_lists(const double* in, const double* out, const unsigned long long* ranks, long long n,
                        int C, unsigned long long* keys, unsigned long long* vals, int sm_count,
                        cudaStream_t s, int* launches);
+// tables: u16 chunk tables (p95_table_entries entries; 0 = the direct scan)
+long long p95_table_entries(const WorkloadArgs& a, long long n);
 void launch_p95_scan(const WorkloadArgs& a, const unsigned long long* keys, const unsigned long long* vals,
-                     long long n, double* p95_in, double* p95_out, cudaStream_t s, int* launches);
+                     long long n, double* p95_in, double* p95_out, unsigned short* tables, cudaStream_t s,
+                     int* launches);
 void launch_workload_stats(const WorkloadArgs& a, long long n, double rate, int integral,
                            const double* sum_in_f, const double* sum_out_f, const double* p95_in,
                            const double* p95_out, double* stats, cudaStream_t s, int* launches);
+// K2 scratch for the block-parallel exact quality sums (entries = tuples x blocks)
+struct QualityScratch {
+    int B;                          // requests per block (quality_block)
+    double* A;                      // approximate block sums
+    short* E;                       // binade per block, -1 = sequential
+    unsigned long long* U;          // units of 2^(e-52) per block
+    unsigned long long* seq_blocks; // optional counter of sequentially folded blocks
+};
+int quality_block(long long n, long long ncand);
 void launch_quality(const double* scores, long long n, int D, const double* thr, long long ncand,
-                    double* qsum, cudaStream_t s, int* launches);
+                    double* qsum, const QualityScratch* q, cudaStream_t s, int* launches);
 
 // ---------------- sort (k_sort.cu)
 void launch_or_and(const unsigned long long* keys, long long n, unsigned long long* out2, cudaStream_t s,

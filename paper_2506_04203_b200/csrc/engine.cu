@@ -199,6 +199,9 @@ struct cg_engine {
     long long conc_lists_max = 1 << 16;  // waves with at most this many listed plans run classes concurrently
     int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
+    int quality_form = 1;  // K2: 1 block-parallel exact (binade units), 0 one fp64 chain per tuple
+    int quality_block = 0; // K2: minimum requests per block (diagnostic; 0 = automatic)
+    int p95_tables = 1;    // K3: chunk tables for large traces (0: the direct column scan)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
@@ -207,7 +210,8 @@ struct cg_engine {
 
     DevBuf d_scores, d_in, d_out;
     DevBuf d_gvals, d_ranks, d_hist, d_flags, d_lk0, d_lv0, d_lk1, d_lv1, d_rshist, d_orax;
-    DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum;
+    DevBuf d_p95tab;
+    DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum, d_qa, d_qe, d_qu, d_qseq;
     DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_ims, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
@@ -1118,7 +1122,9 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
     const unsigned long long* sv = par ? lv1 : lv0;
     double* p95i = E.d_wp95i.as<double>(R.total);
     double* p95o = E.d_wp95o.as<double>(R.total);
-    launch_p95_scan(wa, sk, sv, n, p95i, p95o, x.s, &x.launches);
+    const long long p95_tab = E.p95_tables ? p95_table_entries(wa, n) : 0;
+    launch_p95_scan(wa, sk, sv, n, p95i, p95o,
+                    p95_tab > 0 ? E.d_p95tab.as<unsigned short>((size_t)p95_tab) : nullptr, x.s, &x.launches);
     double* sinf = E.d_wsinf.as<double>(R.total);
     double* soutf = E.d_wsoutf.as<double>(R.total);
     if (!R.integral)
@@ -1143,7 +1149,17 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
     double* dthr = E.d_thr.as<double>(thr.size());
     x.h2d(dthr, thr.data(), (size_t)nq * D * sizeof(double));
     double* qsum = E.d_qsum.as<double>(nq);
-    launch_quality(t.scores, n, D, dthr, nq, qsum, x.s, &x.launches);
+    QualityScratch qs{};
+    if (E.quality_form == 1) {
+        qs.B = std::max(quality_block(n, nq), E.quality_block);  // option: larger blocks (multi-tile path)
+        const size_t ent = (size_t)nq * (size_t)((n + qs.B - 1) / qs.B);
+        qs.A = E.d_qa.as<double>(ent);
+        qs.E = E.d_qe.as<short>(ent);
+        qs.U = E.d_qu.as<unsigned long long>(ent);
+        qs.seq_blocks = E.d_qseq.as<unsigned long long>(1);
+        CG_CUDA(cudaMemsetAsync(qs.seq_blocks, 0, 8, x.s));
+    }
+    launch_quality(t.scores, n, D, dthr, nq, qsum, E.quality_form == 1 ? &qs : nullptr, x.s, &x.launches);
     CG_CUDA(cudaEventRecord(E.ev[3], x.s));
 
     R.stats.resize((size_t)R.total * 5);
@@ -1151,7 +1167,13 @@ RoutingOut route_all(SweepCtx& x, const TraceDev& t, const std::vector<std::vect
     x.d2h(R.stats.data(), stats, R.stats.size() * 8);
     x.d2h(R.count.data(), wa.count, R.count.size() * 8);
     if (extra_thresholds) x.d2h(&R.z2_qsum, qsum + R.ntuples, 8);
+    unsigned long long qseq = 0;
+    if (qs.seq_blocks) x.d2h(&qseq, qs.seq_blocks, 8);
     x.sync();
+    if (qs.seq_blocks) {
+        x.st.quality_blocks += nq * ((n + qs.B - 1) / qs.B);
+        x.st.quality_blocks_seq += (long long)qseq;
+    }
     float m_k1 = 0, m_route = 0, m_q = 0;
     CG_CUDA(cudaEventElapsedTime(&m_k1, E.ev[0], E.ev[1]));
     CG_CUDA(cudaEventElapsedTime(&m_route, E.ev[0], E.ev[2]));
@@ -1881,6 +1903,9 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         const std::string k(key);
         if (k == "prune") e->prune = value ? 1 : 0;
         else if (k == "k1_form") e->k1_form = (int)value;
+        else if (k == "quality_form") e->quality_form = value ? 1 : 0;
+        else if (k == "p95_tables") e->p95_tables = value ? 1 : 0;
+        else if (k == "quality_block") e->quality_block = (int)std::min<int64_t>(1 << 30, std::max<int64_t>(0, value));
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;

@@ -941,6 +941,127 @@ __global__ void k_p95_scan(WorkloadArgs a, const unsigned long long* __restrict_
     }
 }
 
+// K3 with chunk tables (large traces): the sorted columns are cut into
+// chunks of P95_CHUNK positions from the top; per chunk a dominance table over
+// the rank cells gives every workload's member count in that chunk
+// (count(m_0..m_{i-1}, top..top) = members of the stage-i workload with prefix
+// m).  A query walks the chunk counts to the chunk holding its need-th largest
+// member and scans only that chunk, instead of ~5% of the column.
+constexpr int P95_CHUNK = 1024;
+
+__global__ void __launch_bounds__(256) k_p95_tables(const unsigned long long* __restrict__ vals, long long n,
+                                                    int D, WorkloadArgs a, long long cells, int nch,
+                                                    unsigned short* __restrict__ tab) {
+    extern __shared__ unsigned int cnt[];
+    const int k = blockIdx.x, tl = blockIdx.y;
+    const int list = tl == 0 ? 0 : 1 + tl;
+    const unsigned long long* V = vals + (long long)list * n;
+    for (long long c = threadIdx.x; c < cells; c += blockDim.x) cnt[c] = 0u;
+    __syncthreads();
+    const long long hi = n - (long long)k * P95_CHUNK;
+    const long long lo = hi - P95_CHUNK > 0 ? hi - P95_CHUNK : 0;
+    for (long long pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) {
+        const unsigned long long pk = V[pos];
+        long long cell = 0;
+        for (int d = 0; d < D; ++d) cell += (long long)((pk >> (16 * d)) & 0xffffull) * a.stride[d];
+        atomicAdd(&cnt[cell], 1u);
+    }
+    __syncthreads();
+    for (int d = 0; d < D; ++d) {  // dominance prefix along each dimension
+        const long long len = a.G[d] + 1;
+        const long long lines = cells / len;
+        for (long long L = threadIdx.x; L < lines; L += blockDim.x) {
+            const long long base = (L / a.stride[d]) * a.stride[d] * len + L % a.stride[d];
+            unsigned run = 0;
+            for (long long j = 0; j < len; ++j) {
+                run += cnt[base + j * a.stride[d]];
+                cnt[base + j * a.stride[d]] = run;
+            }
+        }
+        __syncthreads();
+    }
+    unsigned short* out = tab + ((long long)tl * nch + k) * cells;
+    for (long long c = threadIdx.x; c < cells; c += blockDim.x) out[c] = (unsigned short)cnt[c];
+}
+
+__global__ void k_p95_query(WorkloadArgs a, const unsigned long long* __restrict__ keys,
+                            const unsigned long long* __restrict__ vals, long long n, int D, long long cells,
+                            int nch, const unsigned short* __restrict__ tab, double* __restrict__ p95_in,
+                            double* __restrict__ p95_out) {
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= 2 * a.total) return;
+    const long long t = warp >> 1;
+    const int which = (int)(warp & 1);
+    const unsigned long long cnt = a.count[t];
+    double* dst = which ? p95_out : p95_in;
+    if (cnt == 0) {
+        if (lane == 0) dst[t] = 0.0;
+        return;
+    }
+    int i = 0;
+    while (i + 1 < a.C && t >= a.wl_off[i + 1]) ++i;
+    long long w = t - a.wl_off[i];
+    unsigned m[4] = {0, 0, 0, 0};
+    long long cell = 0;
+    for (int d = 0; d < D; ++d) {
+        if (d < i) {
+            m[d] = (unsigned)(w % a.G[d]);
+            w /= a.G[d];
+            cell += (long long)m[d] * a.stride[d];
+        } else {
+            cell += (long long)a.G[d] * a.stride[d];
+        }
+    }
+    const int list = which ? 1 + i : 0;
+    const unsigned long long* K = keys + (long long)list * n;
+    const unsigned long long* V = vals + (long long)list * n;
+    long long need = (long long)cnt - p95_index((long long)cnt);  // the need-th largest member
+    if (i == 0) {
+        if (lane == 0) dst[t] = key_to_dbl(K[n - need]);
+        return;
+    }
+    const int tl = which ? i : 0;
+    const unsigned short* T = tab + (long long)tl * nch * cells + cell;
+    int kc = -1;
+    for (int k0 = 0; k0 < nch && kc < 0; k0 += 32) {
+        const int k = k0 + lane;
+        unsigned c = k < nch ? (unsigned)T[(long long)k * cells] : 0u;
+        unsigned incl = c;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= need);
+        if (hit) {
+            const int L = __ffs(hit) - 1;
+            need -= (long long)__shfl_sync(0xffffffffu, incl - c, L);
+            kc = k0 + L;
+        } else {
+            need -= (long long)__shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    const long long top = n - 1 - (long long)kc * P95_CHUNK;  // first position of the chunk, descending
+    for (long long base = 0; base < P95_CHUNK; base += 32) {
+        const long long pos = top - base - lane;
+        bool member = false;
+        if (pos >= 0 && base + lane < P95_CHUNK) {
+            const unsigned long long pk = V[pos];
+            member = true;
+            for (int d = 0; d < i; ++d) member &= ((unsigned)((pk >> (16 * d)) & 0xffffu) <= m[d]);
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, member);
+        const int c = __popc(b);
+        if (c >= need) {
+            const int L = __fns(b, 0, (int)need);
+            if (lane == 0) dst[t] = key_to_dbl(K[top - base - L]);
+            return;
+        }
+        need -= c;
+    }
+}
+
 // WorkloadStats per (stage, prefix): stats_over (routing.cpp:19-38) plus the
 // rate scaling of route_trace (routing.cpp:84-90).
 __global__ void k_workload_stats(WorkloadArgs a, long long n, double rate, int integral,
@@ -1018,6 +1139,279 @@ __global__ void __launch_bounds__(QT_THREADS) k_quality(const double* __restrict
         }
     }
     if (c < ncand) qsum[c] = sum;
+}
+
+
+// ---------------------------------------------------------------------------
+// K2, block-parallel and still bit-exact.  The reference's quality is the
+// trace-order fold s <- fl(s + a_r) of each tuple's accepted scores
+// (routing.cpp:79).  While s stays in one binade [2^e, 2^(e+1)) every partial
+// sum is a multiple of u = 2^(e-52), so for a_r >= 0 each step adds exactly
+// u * rn(a_r / u) -- unless a_r / u is a tie (then the parity of s decides).
+// A block of requests therefore advances s by an integer D(e) of units that
+// does not depend on s, and the fold over blocks is an integer chain:
+//   Q1  per (tuple, block): approximate block sum (any order) and a flag for
+//       negative / non-finite scores;
+//   Q2  per tuple: approximate prefix -> the binade each block will run in,
+//       or "sequential" when a block may cross a binade (or s = 0, or flagged);
+//   Q3  per (tuple, block) in one binade: D = sum of rn(a_r / u) (integer
+//       shifts of the scores' bits), "sequential" on any tie or a_r >= s;
+//   Q4  per tuple: the exact chain -- fast blocks check that s is in the
+//       binade and stays below 2^(e+1) (partial sums are monotone), then
+//       s += u * D exactly; every other block is folded request by request
+//       with __dadd_rn, as the reference does.
+// Sequential blocks are the first (s = 0), ~log2(blocks) binade crossings and
+// the rare ties, so the fp64 add chain shrinks from n to a few blocks.
+constexpr int QX_THREADS = 256;   // tuples per CTA of Q1 / Q3
+constexpr int QX_TILE = 1024;     // requests staged per shared-memory tile
+constexpr short QX_SEQ = -1;      // block folded sequentially in Q4
+
+template <int D>
+__device__ __forceinline__ double accepted_score(const double* __restrict__ row, const double* h) {
+    double a = row[D];
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) a = (row[d] >= h[d]) ? row[d] : a;
+    return a;
+}
+
+template <int D>
+__device__ __forceinline__ void stage_tile(const double* __restrict__ scores, long long n, long long base, int len,
+                                           double* tile) {
+    constexpr int C = D + 1;
+    for (int i = 0; i < C; ++i)
+        for (int k = threadIdx.x; k < len; k += blockDim.x) tile[k * C + i] = scores[(long long)i * n + base + k];
+}
+
+// Q1: grid (blocks, tuple groups); approximate block sums, NaN marks a block
+// with a negative, -0.0 or non-finite accepted score.
+template <int D>
+__global__ void __launch_bounds__(QX_THREADS) k_qx_approx(const double* __restrict__ scores, long long n, int B,
+                                                          const double* __restrict__ thr, long long ncand, int nb,
+                                                          double* __restrict__ A) {
+    constexpr int C = D + 1;
+    extern __shared__ double qtile[];
+    const int b = blockIdx.x;
+    const long long c = (long long)blockIdx.y * QX_THREADS + threadIdx.x;
+    double h[D > 0 ? D : 1];
+#pragma unroll
+    for (int d = 0; d < D; ++d) h[d] = c < ncand ? thr[c * D + d] : 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    bool bad = false;
+    const long long b0 = (long long)b * B;
+    const long long b1 = b0 + B < n ? b0 + B : n;
+    for (long long base = b0; base < b1; base += QX_TILE) {
+        const int len = (int)(b1 - base < QX_TILE ? b1 - base : QX_TILE);
+        __syncthreads();
+        stage_tile<D>(scores, n, base, len, qtile);
+        __syncthreads();
+        int k = 0;
+        for (; k + 4 <= len; k += 4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double a = accepted_score<D>(qtile + (k + j) * C, h);
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+                bad |= (bits >> 63) != 0ull || (bits >> 52) == 2047ull;
+                acc[j] += a;
+            }
+        }
+        for (; k < len; ++k) {
+            const double a = accepted_score<D>(qtile + k * C, h);
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+            bad |= (bits >> 63) != 0ull || (bits >> 52) == 2047ull;
+            acc[0] += a;
+        }
+    }
+    if (c < ncand) A[c * nb + b] = bad ? __longlong_as_double(0x7ff8000000000000ll) : (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// Q2: one warp per tuple; the binade (biased exponent) each block runs in.
+__global__ void k_qx_binades(const double* __restrict__ A, long long ncand, int nb, short* __restrict__ E) {
+    const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= ncand) return;
+    double run = 0.0;  // approximate prefix before this chunk
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+        const int b = b0 + lane;
+        const double a = b < nb ? A[c * nb + b] : 0.0;
+        const bool bad = a != a;
+        double incl = bad ? 0.0 : a;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const double lo = (run + incl - (bad ? 0.0 : a)) * (1.0 - 1e-9);
+        const double hi = (run + incl) * (1.0 + 1e-9);
+        short e = QX_SEQ;
+        if (!bad && lo > 0.0) {
+            const int elo = (int)(((unsigned long long)__double_as_longlong(lo) >> 52) & 2047ull);
+            const int ehi = (int)(((unsigned long long)__double_as_longlong(hi) >> 52) & 2047ull);
+            if (elo == ehi && elo > 52 && elo < 2047) e = (short)elo;  // u = 2^(e-52) normal
+        }
+        if (b < nb) E[c * nb + b] = e;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
+// Q3: grid (blocks, tuple groups); units of u = 2^(e-52) added by each block.
+template <int D>
+__global__ void __launch_bounds__(QX_THREADS) k_qx_units(const double* __restrict__ scores, long long n, int B,
+                                                         const double* __restrict__ thr, long long ncand, int nb,
+                                                         short* __restrict__ E, unsigned long long* __restrict__ U) {
+    constexpr int C = D + 1;
+    extern __shared__ double qtile[];
+    const int b = blockIdx.x;
+    const long long c = (long long)blockIdx.y * QX_THREADS + threadIdx.x;
+    const bool live = c < ncand;
+    const int eb = live ? (int)E[c * nb + b] : QX_SEQ;
+    if (__syncthreads_and(eb == QX_SEQ)) return;  // the whole CTA folds this block sequentially
+    double h[D > 0 ? D : 1];
+#pragma unroll
+    for (int d = 0; d < D; ++d) h[d] = live ? thr[c * D + d] : 0.0;
+    unsigned long long sum = 0ull;
+    bool seq = eb == QX_SEQ;
+    const long long b0 = (long long)b * B;
+    const long long b1 = b0 + B < n ? b0 + B : n;
+    for (long long base = b0; base < b1; base += QX_TILE) {
+        const int len = (int)(b1 - base < QX_TILE ? b1 - base : QX_TILE);
+        __syncthreads();
+        stage_tile<D>(scores, n, base, len, qtile);
+        __syncthreads();
+        if (seq) continue;
+        for (int k = 0; k < len; ++k) {
+            const double a = accepted_score<D>(qtile + k * C, h);
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(a);
+            const int ea = (int)(bits >> 52);  // sign bit is 0 here (Q1 checked)
+            const unsigned long long m = (bits & 0xfffffffffffffull) | (ea ? (1ull << 52) : 0ull);
+            const int sh = eb - (ea ? ea : 1);
+            seq |= sh <= 0;  // a >= 2^e: s + a leaves the binade
+            if (sh > 0 && sh < 64) {
+                const unsigned long long r = m << (64 - sh);
+                seq |= r == (1ull << 63);  // tie: the parity of s decides
+                sum += (m >> sh) + (r > (1ull << 63) ? 1ull : 0ull);
+            }
+        }
+    }
+    if (!live) return;
+    if (seq) E[c * nb + b] = QX_SEQ;
+    else U[c * nb + b] = sum;
+}
+
+// Q4: one warp per tuple, the exact chain over blocks.  The warp reads 32
+// blocks' (binade, units) at once; a chunk whose blocks all run in the
+// current binade advances s by the warp's integer sum of their units in one
+// step.  Otherwise the chunk is walked block by block: fast blocks as integer
+// steps, the rest folded request by request -- the lanes load and select 32
+// accepted scores at a time (independent of s), lane 0's chain adds them in
+// trace order with __dadd_rn.
+template <int D>
+__device__ double qx_fold_block(const double* __restrict__ scores, long long n, long long b0, long long b1,
+                                const double* h, double s, int lane) {
+    constexpr int C = D + 1;
+    for (long long r0 = b0; r0 < b1; r0 += 32) {
+        const long long r = r0 + lane;
+        double a = 0.0;
+        if (r < b1) {
+            double row[C];
+#pragma unroll
+            for (int i = 0; i < C; ++i) row[i] = scores[(long long)i * n + r];
+            a = accepted_score<D>(row, h);
+        }
+        const int cnt = (int)(b1 - r0 < 32 ? b1 - r0 : 32);
+        if (cnt == 32) {
+            double v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __shfl_sync(0xffffffffu, a, j);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s = __dadd_rn(s, v[j]);
+        } else {
+            for (int j = 0; j < cnt; ++j) s = __dadd_rn(s, __shfl_sync(0xffffffffu, a, j));
+        }
+    }
+    return s;
+}
+
+// s in [2^e, 2^(e+1)) (biased e) and s + units * 2^(e-52) < 2^(e+1): the exact
+// result, else a negative value.
+__device__ __forceinline__ double qx_units_step(double s, int eb, unsigned long long units) {
+    const double u = __longlong_as_double((long long)(eb - 52) << 52);
+    const double lo = __longlong_as_double((long long)eb << 52);
+    if (!(s >= lo && s < 2.0 * lo)) return -1.0;
+    const unsigned long long su = (unsigned long long)__double2ll_rn(__ddiv_rn(s, u));  // exact
+    const unsigned long long t = su + units;
+    if (t >= (1ull << 53) || t < su) return -1.0;
+    return __dmul_rn((double)(long long)t, u);  // exact: t < 2^53
+}
+
+template <int D>
+__global__ void k_qx_chain(const double* __restrict__ scores, long long n, int B,
+                           const double* __restrict__ thr, long long ncand, int nb,
+                           const short* __restrict__ E, const unsigned long long* __restrict__ U,
+                           double* __restrict__ qsum, unsigned long long* __restrict__ seq_blocks) {
+    const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (c >= ncand) return;
+    double h[D > 0 ? D : 1];
+#pragma unroll
+    for (int d = 0; d < D; ++d) h[d] = thr[c * D + d];
+    double s = 0.0;
+    unsigned long long nseq = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+        const int b = b0 + lane;
+        const int eb = b < nb ? (int)E[c * nb + b] : -2;  // -2: past the end
+        const unsigned long long uu = (b < nb && eb >= 0) ? U[c * nb + b] : 0ull;
+        // fast chunk: every live block in the binade of s
+        const int es = s > 0.0 ? (int)(((unsigned long long)__double_as_longlong(s) >> 52) & 2047ull) : -3;
+        if (__all_sync(0xffffffffu, eb == es || eb == -2)) {
+            unsigned long long tot = uu;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+            const double t = qx_units_step(s, es, tot);  // every live unit sum < 2^53: no wrap
+            if (t >= 0.0) {
+                s = t;
+                continue;
+            }
+        }
+        const int cnt = nb - b0 < 32 ? nb - b0 : 32;
+        for (int j = 0; j < cnt; ++j) {
+            const int ej = __shfl_sync(0xffffffffu, eb, j);
+            const unsigned long long uj = __shfl_sync(0xffffffffu, uu, j);
+            if (ej >= 0) {
+                const double t = qx_units_step(s, ej, uj);
+                if (t >= 0.0) {
+                    s = t;
+                    continue;
+                }
+            }
+            ++nseq;
+            const long long r0 = (long long)(b0 + j) * B;
+            s = qx_fold_block<D>(scores, n, r0, r0 + B < n ? r0 + B : n, h, s, lane);
+        }
+    }
+    if (lane == 0) {
+        qsum[c] = s;
+        if (seq_blocks) atomicAdd(seq_blocks, nseq);
+    }
+}
+
+template <int D>
+void launch_qx(const double* scores, long long n, const double* thr, long long ncand, double* qsum,
+               const QualityScratch& q, cudaStream_t s, int* launches) {
+    const int nb = (int)((n + q.B - 1) / q.B);
+    const dim3 grid((unsigned)nb, (unsigned)((ncand + QX_THREADS - 1) / QX_THREADS));
+    const size_t smem = (size_t)QX_TILE * (D + 1) * sizeof(double);
+    CG_CUDA(cudaFuncSetAttribute(k_qx_approx<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CG_CUDA(cudaFuncSetAttribute(k_qx_units<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_qx_approx<D><<<grid, QX_THREADS, smem, s>>>(scores, n, q.B, thr, ncand, nb, q.A);
+    CG_LAUNCH_CHECK();
+    k_qx_binades<<<(unsigned)((ncand * 32 + 255) / 256), 256, 0, s>>>(q.A, ncand, nb, q.E);
+    CG_LAUNCH_CHECK();
+    k_qx_units<D><<<grid, QX_THREADS, smem, s>>>(scores, n, q.B, thr, ncand, nb, q.E, q.U);
+    CG_LAUNCH_CHECK();
+    k_qx_chain<D><<<(unsigned)((ncand * 32 + 127) / 128), 128, 0, s>>>(scores, n, q.B, thr, ncand, nb, q.E, q.U,
+                                                                       qsum, q.seq_blocks);
+    CG_LAUNCH_CHECK();
+    if (launches) *launches += 4;
 }
 
 }  // namespace
@@ -1213,10 +1607,33 @@ void launch_make_lists(const double* in, const double* out, const unsigned long 
     if (launches) ++*launches;
 }
 
+long long p95_table_entries(const WorkloadArgs& a, long long n) {
+    const int D = a.C - 1;
+    long long cells = 1;
+    for (int d = 0; d < D; ++d) cells *= a.G[d] + 1;
+    if (D == 0 || cells > 16384 || n < 65536) return 0;  // the direct scan
+    return (long long)a.C * ((n + P95_CHUNK - 1) / P95_CHUNK) * cells;
+}
+
 void launch_p95_scan(const WorkloadArgs& a, const unsigned long long* keys,
                      const unsigned long long* vals, long long n, double* p95_in, double* p95_out,
-                     cudaStream_t s, int* launches) {
+                     unsigned short* tables, cudaStream_t s, int* launches) {
     const long long warps = 2 * a.total;
+    if (tables && p95_table_entries(a, n) > 0) {
+        const int D = a.C - 1;
+        long long cells = 1;
+        for (int d = 0; d < D; ++d) cells *= a.G[d] + 1;
+        const int nch = (int)((n + P95_CHUNK - 1) / P95_CHUNK);
+        const size_t smem = (size_t)cells * 4;
+        CG_CUDA(cudaFuncSetAttribute(k_p95_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_p95_tables<<<dim3((unsigned)nch, (unsigned)a.C), 256, smem, s>>>(vals, n, D, a, cells, nch, tables);
+        CG_LAUNCH_CHECK();
+        k_p95_query<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(a, keys, vals, n, D, cells, nch, tables,
+                                                                         p95_in, p95_out);
+        CG_LAUNCH_CHECK();
+        if (launches) *launches += 2;
+        return;
+    }
     k_p95_scan<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(a, keys, vals, n, p95_in, p95_out);
     CG_LAUNCH_CHECK();
     if (launches) ++*launches;
@@ -1231,8 +1648,26 @@ void launch_workload_stats(const WorkloadArgs& a, long long n, double rate, int 
     if (launches) ++*launches;
 }
 
+int quality_block(long long n, long long ncand) {
+    // requests per block: entries (tuples x blocks) stay <= 2^24 (~300 MB of scratch)
+    int B = QX_TILE;
+    while ((double)ncand * (double)((n + B - 1) / B) > (double)(1 << 24) && B < (1 << 30)) B *= 2;
+    return B;
+}
+
 void launch_quality(const double* scores, long long n, int D, const double* thr, long long ncand,
-                    double* qsum, cudaStream_t s, int* launches) {
+                    double* qsum, const QualityScratch* q, cudaStream_t s, int* launches) {
+    if (ncand <= 0 || n <= 0) return;
+    if (q) {  // block-parallel exact form
+        switch (D) {
+            case 0: launch_qx<0>(scores, n, thr, ncand, qsum, *q, s, launches); return;
+            case 1: launch_qx<1>(scores, n, thr, ncand, qsum, *q, s, launches); return;
+            case 2: launch_qx<2>(scores, n, thr, ncand, qsum, *q, s, launches); return;
+            case 3: launch_qx<3>(scores, n, thr, ncand, qsum, *q, s, launches); return;
+            case 4: launch_qx<4>(scores, n, thr, ncand, qsum, *q, s, launches); return;
+            default: throw EngineError(101, "GPU engine supports up to 5 cascade stages");
+        }
+    }
     const unsigned blocks = (unsigned)((ncand + QT_THREADS - 1) / QT_THREADS);
     switch (D) {
         case 0: k_quality<0><<<blocks, QT_THREADS, 0, s>>>(scores, n, thr, ncand, qsum); break;

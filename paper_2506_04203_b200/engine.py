@@ -107,7 +107,8 @@ class SweepStats(ctypes.Structure):
         "plans_stable", "plans_simulated_full", "plans_pruned", "plans_bound_skipped", "plans_seeded", "plans_overflow", "request_steps",
         "h2d_bytes", "d2h_bytes")] + [("num_ranks", ctypes.c_int32), ("gpu_launches", ctypes.c_int32)] + \
         [(n, ctypes.c_double) for n in ("ms_total", "ms_route", "ms_quality", "ms_rows", "ms_solve",
-                                        "ms_k1", "k1_bytes", "ms_k4")] + [("collectives", ctypes.c_int64)]
+                                        "ms_k1", "k1_bytes", "ms_k4")] + [("collectives", ctypes.c_int64), ("quality_blocks", ctypes.c_int64),
+                                                           ("quality_blocks_seq", ctypes.c_int64)]
 
 
 class SweepResultC(ctypes.Structure):

@@ -46,7 +46,18 @@ static int64_t run_rule(rowctx* x, int dp, double U, int K, int every, int rule,
                     svc = v < svc ? v : svc;
                 }
                 double lb = svc * (1.0 - 1e-12) - 1e-12 * x->arr[n - 1];
-                if (rule == 1 && amin > x->arr[j]) lb += (amin - x->arr[j]) * (1.0 - 1e-12);
+                if (rule == 1 && amin > x->arr[j]) {
+                    /* B': per replica, the wait until its current release plus its own service */
+                    double b2 = INFINITY;
+                    for (int r = 0; r < dp; ++r) {
+                        const int s = x->rep_shape[r];
+                        const double wv = x->avail[r] > x->arr[j] ? x->avail[r] - x->arr[j] : 0.0;
+                        const double v = wv + x->prefill[s] + x->outs[j] * x->decode[s];
+                        b2 = v < b2 ? v : b2;
+                    }
+                    b2 = b2 * (1.0 - 1e-12) - 1e-12 * x->arr[n - 1];
+                    lb = b2 > lb ? b2 : lb;
+                }
                 if (lb > U) ++fut;
             }
             if (ab + fut >= K) {
