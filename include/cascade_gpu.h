@@ -174,6 +174,9 @@ typedef struct cg_sweep_stats {
     int64_t collectives;          /* bound exchanges (all-gathers) of a sharded call, final merge excluded */
     int64_t quality_blocks;       /* K2 (tuple, request block) pairs */
     int64_t quality_blocks_seq;   /* of those, folded request by request (binade crossings, ties, s = 0) */
+    int64_t waves_total;          /* K4 filter waves of the plan lists */
+    int64_t waves_run;            /* of those, run (< waves_total only under max_waves / wave_stride) */
+    int64_t plans_in_waves;       /* plan indices covered by the waves run (64-plan chunks) */
 } cg_sweep_stats;
 
 /* cascade::outerplan::SweepResult (outerplan.hpp:73-80), flattened. */
@@ -245,7 +248,9 @@ void* cg_engine_stream(cg_engine* engine);
 /* Engine options.  None changes any result (tests/test_gpu_parity.py checks
  * each); they select work order and kernel forms:
  *   "prune"            1 (default) exact p95-bound elimination in K4; 0 simulates every stable plan
- *   "k4_pack"          3 (default) lane-major k_lane for dp <= 32; 0-2 group-per-plan k_sim forms
+ *   "k4_pack"          3 (default) lane-major k_lane for dp <= 32, one lane per plan (R = 4/8/16/32
+ *                      replicas per lane); 4: W = 1/1/2/1 lanes per plan, R = 4/8/8/32; 5: W = 1/1/2/4,
+ *                      R = 4/8/8/8; 0-2 group-per-plan k_sim forms
  *   "pilot"            1 (default) best-estimate plan per (row, budget) simulated first
  *   "pilot_merge"      1 (default) pilot launch grouping (0 per class, 2 one launch)
  *   "pilot_min_plans"  0 (default) rows with fewer plans get no pilot
@@ -257,6 +262,8 @@ void* cg_engine_stream(cg_engine* engine);
  *                      replica-count classes concurrently on four streams (0: never)
  *   "quality_form"     1 (default) block-parallel exact K2 quality sums; 0 one fp64 add chain per tuple
  *   "p95_tables"       1 (default) K3 chunk tables for traces >= 65536 requests; 0 direct column scans
+ *   "max_waves", "wave_stride"  rate sampling only: run at most max_waves filter waves, every
+ *                      wave_stride-th one; the result is then PARTIAL (stats.waves_run < waves_total)
  *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle",
  *   "quality_block" (diagnostic)
  * Unknown keys return CG_ERR_INVALID_INPUT. */

@@ -202,6 +202,8 @@ struct cg_engine {
     int quality_form = 1;  // K2: 1 block-parallel exact (binade units), 0 one fp64 chain per tuple
     int quality_block = 0; // K2: minimum requests per block (diagnostic; 0 = automatic)
     int p95_tables = 1;    // K3: chunk tables for large traces (0: the direct column scan)
+    long long max_waves = 0;   // rate sampling: stop after this many filter waves (0 = all; result partial)
+    long long wave_stride = 1; // rate sampling: run every wave_stride-th wave only (result partial)
     int k1_form = 0;   // 0 auto (TMA ring), 1 tiled/u64 forms only, 2 u32 register form (3: 1 block/SM)
     int item_plans = 128;
     long long ovf_cap = 1 << 20;
@@ -312,7 +314,7 @@ int row_class(const HostPlanSpace& sp, int N) {
 void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vector<HostPlanSpace>& hs,
                    const cg_hardware& hw, const cg_cost_params& q, int N) {
     cg_engine& E = x.E;
-    set_k4_pack(E.k4_pack == 3 && q.queueing_sim_requests > 65535 ? 1 : E.k4_pack);  // k_lane rings hold u16 request indices
+    set_k4_pack(E.k4_pack >= 3 && q.queueing_sim_requests > 65535 ? 1 : E.k4_pack);  // k_lane rings hold u16 request indices
     const int nrows = (int)rows.size();
     if (rows.size() >= (1ull << (64 - kItemPlanBits)))
         fail(CG_ERR_UNSUPPORTED, "too many unique rows for the 20-bit row field of a work item");
@@ -694,8 +696,18 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                 pilot_join = false;
             }
         }
+        long long wave_no = -1, waves_run = 0;
         for (unsigned long long w0 = 0; w0 < max_chunks; w0 += wave_chunks) {
             const unsigned long long nch = w0 < my_chunks ? std::min<unsigned long long>(wave_chunks, my_chunks - w0) : 0;
+            ++wave_no;
+            ++x.st.waves_total;
+            // rate sampling (diagnostic; the result is then partial): every
+            // wave_stride-th wave, at most max_waves of them
+            if (E.wave_stride > 1 && wave_no % E.wave_stride != 0) continue;
+            if (E.max_waves > 0 && waves_run >= E.max_waves) continue;
+            ++waves_run;
+            ++x.st.waves_run;
+            x.st.plans_in_waves += (long long)nch * chunk;
             CG_CUDA(cudaMemsetAsync(lcount, 0, 7 * 8, x.s));
             FilterArgs fa{};
             fa.N = N;
@@ -1905,6 +1917,8 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k1_form") e->k1_form = (int)value;
         else if (k == "quality_form") e->quality_form = value ? 1 : 0;
         else if (k == "p95_tables") e->p95_tables = value ? 1 : 0;
+        else if (k == "max_waves") e->max_waves = std::max<int64_t>(0, value);
+        else if (k == "wave_stride") e->wave_stride = std::max<int64_t>(1, value);
         else if (k == "quality_block") e->quality_block = (int)std::min<int64_t>(1 << 30, std::max<int64_t>(0, value));
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;

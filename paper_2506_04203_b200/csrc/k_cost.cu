@@ -782,12 +782,17 @@ struct LaneTraits {
     // 128-thread blocks per SM within shared memory); deeper queues overflow
     // to the DEEP re-run.  (Four blocks per SM -- 128 registers, half the
     // slots -- measured slower: C3 K4 746 -> 795 ms.)
-    static constexpr int CAP = R <= 4 ? 32 : (W == 1 ? 8 : 16);
+    // R = 16 / 32 (one lane holds a whole dp <= 32 plan): 4 slots, deeper
+    // queues overflow to the DEEP re-run; 2-warp blocks pack shared memory
+    static constexpr int CAP = R <= 4 ? 32 : (R <= 8 ? (W == 1 ? 8 : 16) : 4);
+    static constexpr int WPB = R >= 16 ? 2 : 4;  // warps per block
     static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
-    static constexpr size_t pd_bytes = (size_t)3 * R * 32 * sizeof(double);  // prefill, decode, head finish
+    // prefill, decode, head-job finish, previous-job finish (per replica slot)
+    static constexpr size_t pd_bytes = (size_t)4 * R * 32 * sizeof(double);
+    static constexpr size_t ht_bytes = (size_t)R * 32 * sizeof(unsigned);  // ring head | tail << 16
     static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
-    static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + hist_bytes + G * sizeof(GroupShared);
+    static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + ht_bytes + hist_bytes + G * sizeof(GroupShared);
 };
 
 // Claims work item `it` into gs; false when the item is rejected (an unstable
@@ -894,7 +899,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
 constexpr unsigned kLaneCheck = 32;  // request-steps between exact-bound prune checks
 
 template <int W, int R>
-__global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimArgs a) {
+__global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimArgs a) {
     using TR = LaneTraits<W, R>;
     constexpr int G = TR::G;
     constexpr int CAP = TR::CAP;
@@ -912,8 +917,16 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
     double* pre_s = reinterpret_cast<double*>(wbase + TR::ring_bytes);
     double* dec_s = pre_s + R * 32;
     double* nd_s = dec_s + R * 32;  // finish time of each replica's head job (INF: none)
-    unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
-    GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::hist_bytes);
+    // finish of the job before each replica's last one (INF: no replica; a
+    // value <= t means the replica holds exactly one job at t).  Only the
+    // winner's slot changes per step, so prev and the ring heads live in
+    // shared memory (one predicated store) rather than in registers (a
+    // select per replica per step).
+    double* prev_s = nd_s + R * 32;
+    unsigned* ht_s = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
+    unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes);
+    GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes +
+                                                      TR::hist_bytes);
     GroupShared& gs = gsa[gid];
 
     const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -937,20 +950,20 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
     const double* Orow = a.tab.O;
     // arrivals / outputs of the pair holding step k and of the next pair (prefetched)
     double2 tq = make_double2(0.0, 0.0), oq = tq, tq2 = tq, oq2 = tq;
-    // per replica: avail = finish of its last job, prev = finish of the job
-    // before it (0 = none); the head job's finish lives in shared memory (nd_s)
-    double avail[R], prev[R];
+    // per replica: avail = finish of its last job (registers: every step's
+    // idle mask reads them all); the head job's finish (nd_s), the previous
+    // job's finish (prev_s) and the ring head/tail (ht_s) live in shared memory
+    double avail[R];
     // W == 1: output tokens of the job at the ring head, loaded one pop ahead
     // (the lanes' rows differ, so a load at pop time would stall on L2)
-    constexpr bool HO = W == 1;
+    constexpr bool HO = W == 1 && R <= 8;
     double ho[R];
-    unsigned ht[R];  // head | tail << 16 of the waiting-job ring
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         avail[r] = INF;
-        prev[r] = INF;
         ho[r] = 0.0;
-        ht[r] = 0;
+        ht_s[r * 32 + lane] = 0u;
+        prev_s[r * 32 + lane] = INF;
     }
     unsigned long long steps = 0, full = 0, pruned = 0, bound = 0;
 
@@ -994,9 +1007,9 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
                         nd_s[r * 32 + lane] = INF;
-                        ht[r] = 0;
+                        ht_s[r * 32 + lane] = 0u;
                         avail[r] = INF;
-                        prev[r] = INF;
+                        prev_s[r * 32 + lane] = INF;
                         if (j < dp) {
                             if (np > 0) {
                                 while (j >= cum) {
@@ -1013,7 +1026,7 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                             pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
                             dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
                             avail[r] = 0.0;
-                            prev[r] = 0.0;
+                            prev_s[r * 32 + lane] = 0.0;
                         }
                     }
                     mcur = 0;  // every replica starts idle (avail 0 <= T[0])
@@ -1080,7 +1093,7 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                 // (costmodel.cpp:262-276) -- no FIFO walk needed.
                 unsigned m1 = 0;
 #pragma unroll
-                for (int r = 0; r < R; ++r) m1 |= (prev[r] <= t) ? (1u << r) : 0u;
+                for (int r = 0; r < R; ++r) m1 |= (busy && prev_s[r * 32 + lane] <= t) ? (1u << r) : 0u;
                 m1 = busy ? m1 : 0u;
                 bool has1;
                 if (W == 1) {
@@ -1102,8 +1115,11 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
                             const bool lz = (lazy >> r) & 1u;
-                            if (lz) nd_s[r * 32 + lane] = avail[r];
-                            ht[r] = lz ? ((ht[r] & 0xffff0000u) | (ht[r] >> 16)) : ht[r];
+                            if (lz) {
+                                nd_s[r * 32 + lane] = avail[r];
+                                const unsigned hr = ht_s[r * 32 + lane];
+                                ht_s[r * 32 + lane] = (hr & 0xffff0000u) | (hr >> 16);
+                            }
                         }
                         lazy = 0;
                     }
@@ -1114,8 +1130,9 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
                             if (!((dep >> r) & 1u)) continue;
-                            const unsigned h = ht[r] & 0xffffu;
-                            const unsigned tl = ht[r] >> 16;
+                            const unsigned hr = ht_s[r * 32 + lane];
+                            const unsigned h = hr & 0xffffu;
+                            const unsigned tl = hr >> 16;
                             const bool more = h != tl;  // the head waiting job enters service
                             double oh = 0.0;
                             if (HO) oh = ho[r];
@@ -1126,7 +1143,7 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                             const double nn = more ? nx : INF;
                             nd_s[r * 32 + lane] = nn;
                             const unsigned h1 = (h + 1u) & 0xffffu;
-                            ht[r] = more ? ((ht[r] & 0xffff0000u) | h1) : ht[r];
+                            if (more) ht_s[r * 32 + lane] = (hr & 0xffff0000u) | h1;
                             if (HO && more && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
                             dep = (nn <= t) ? dep : (dep & ~(1u << r));
                         }
@@ -1136,7 +1153,8 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
-                        const unsigned c = (((ht[r] >> 16) - ht[r]) & 0xffffu) + (nd_s[r * 32 + lane] < INF ? 1u : 0u);
+                        const unsigned hr = ht_s[r * 32 + lane];
+                        const unsigned c = (((hr >> 16) - hr) & 0xffffu) + (nd_s[r * 32 + lane] < INF ? 1u : 0u);
                         kk[r] = (j < dp) ? ((c << 9) | (unsigned)j) : 0xffffffffu;
                     }
 #pragma unroll
@@ -1156,24 +1174,17 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                     }
                 }
                 if (busy) {
-                    // avail / ring state of replica rr: select tree on rr's bits
+                    // avail of replica rr: select tree on rr's bits; its ring state from shared memory
                     double av[R];
-                    unsigned hv[R];
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        av[r] = avail[r];
-                        hv[r] = ht[r];
-                    }
+                    for (int r = 0; r < R; ++r) av[r] = avail[r];
 #pragma unroll
                     for (int w = 1; w < R; w <<= 1) {
                         const bool hi = (rr & w) != 0;
 #pragma unroll
-                        for (int r = 0; r + w < R; r += 2 * w) {
-                            av[r] = hi ? av[r + w] : av[r];
-                            hv[r] = hi ? hv[r + w] : hv[r];
-                        }
+                        for (int r = 0; r + w < R; r += 2 * w) av[r] = hi ? av[r + w] : av[r];
                     }
-                    H = hv[0];
+                    H = ht_s[rr * 32 + lane];
                     start = av[0];  // > t: std::max(t, avail)
                     const int pidx = rr * 32 + lane;
                     fin = __dadd_rn(__dadd_rn(start, pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
@@ -1197,13 +1208,14 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
                 H += push ? (1u << 16) : 0u;
                 ovf |= push && ((((H >> 16) - H) & 0xffffu) > (unsigned)CAP);
                 lazy |= (me && idle) ? (1u << rr) : 0u;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const bool hit = me && r == rr;
-                    prev[r] = hit ? avail[r] : prev[r];
-                    avail[r] = hit ? fin : avail[r];
-                    ht[r] = hit ? H : ht[r];
+                // prev = start: the old finish when busy; when idle any value
+                // <= t (every later test is prev <= t' with t' >= t)
+                if (me) {
+                    prev_s[rr * 32 + lane] = start;
+                    ht_s[rr * 32 + lane] = H;
                 }
+#pragma unroll
+                for (int r = 0; r < R; ++r) avail[r] = (me && r == rr) ? fin : avail[r];
                 if (HO && first) {  // the job is the head of an empty ring (rarer than a step)
 #pragma unroll
                     for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
@@ -1220,21 +1232,19 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
             k += run ? 1 : 0;
             status = (run && k == n_req) ? ST_FINISH : status;
         };
+        // k == u (mod 4) on every running lane: steps come in (even, odd)
+        // pairs; after the even step the pair registers shift and the pair
+        // after next is prefetched
 #pragma unroll 1
-        for (int u = 0; u < UNROLL; ++u) {
-            // k == u (mod 4) on every running lane, so the parity is warp-uniform
-            const bool odd = (u & 1) != 0;
-            const double t = odd ? tq.y : tq.x;
-            const double o = odd ? oq.y : oq.x;
-            const double tn1 = odd ? tq2.x : tq.y;  // the next request's arrival
-            if (odd) {
-                tq = tq2;
-                oq = oq2;
-                const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
-                tq2 = *reinterpret_cast<const double2*>(Trow + kp);
-                oq2 = *reinterpret_cast<const double2*>(Orow + kp);
-            }
-            step(t, o, tn1);
+        for (int u = 0; u < UNROLL; u += 2) {
+            step(tq.x, oq.x, tq.y);
+            const double t1 = tq.y, o1 = oq.y, tn1 = tq2.x;  // tn1: the next request's arrival
+            tq = tq2;
+            oq = oq2;
+            const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
+            tq2 = *reinterpret_cast<const double2*>(Trow + kp);
+            oq2 = *reinterpret_cast<const double2*>(Orow + kp);
+            step(t1, o1, tn1);
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
@@ -1337,16 +1347,16 @@ __global__ void __launch_bounds__(128, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimA
 template <int W, int R>
 void launch_lane_t(const SimArgs& a, int sm_count, cudaStream_t s, int* launches, int* grid_out) {
     using TR = LaneTraits<W, R>;
-    const size_t smem = TR::bytes_per_warp * 4;
+    const size_t smem = TR::bytes_per_warp * TR::WPB;
     auto kern = k_lane<W, R>;
     CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    CG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TR::WPB * 32, smem));
     if (per_sm < 1) per_sm = 1;
     const int grid = sm_count * per_sm;
     if (grid_out) *grid_out = grid;
     if (a.nitems == 0) return;
-    kern<<<grid, 128, smem, s>>>(a);
+    kern<<<grid, TR::WPB * 32, smem, s>>>(a);
     CG_LAUNCH_CHECK();
     if (launches) ++*launches;
 }
@@ -1666,16 +1676,18 @@ SimGeometry sim_geometry(int cls, int mode, int sm_count) {
 //   0: one replica per lane, W = 4/8/16/32 lanes for dp <= 4/8/16/32
 //   1: two replicas per lane from dp > 4 on (more plans per warp)
 //   2: up to four replicas per lane
-//   3: lane-major kernels (k_lane) for dp <= 32: W = 1/1/2/4 lanes with
-//      R = 4/8/8/8 replicas per lane
-static int g_pack = 0;
-void set_k4_pack(int p) { g_pack = p < 0 ? 0 : (p > 3 ? 3 : p); }
+//   3: lane-major kernels (k_lane) for dp <= 32, one lane per plan: R = 4/8/16/32
+//      replicas per lane (default; C3 K4 890 -> 670 ms against 5)
+//   4: k_lane with W = 1/1/2/1 lanes per plan, R = 4/8/8/32
+//   5: k_lane with W = 1/1/2/4, R = 4/8/8/8 (round 1)
+static thread_local int g_pack = 0;  // per host thread: engines of a multi-device group run concurrently
+void set_k4_pack(int p) { g_pack = p < 0 ? 0 : (p > 5 ? 5 : p); }
 
 void class_shape(int cls, int* W, int* R) {
-    static const int Ws[4][7] = {{4, 8, 16, 32, 32, 32, 32}, {4, 4, 8, 16, 32, 32, 32}, {4, 4, 4, 8, 32, 32, 32},
-                                 {1, 1, 2, 4, 32, 32, 32}};
-    static const int Rs[4][7] = {{1, 1, 1, 1, 2, 4, 8}, {1, 2, 2, 2, 2, 4, 8}, {1, 2, 4, 4, 2, 4, 8},
-                                 {4, 8, 8, 8, 2, 4, 8}};
+    static const int Ws[6][7] = {{4, 8, 16, 32, 32, 32, 32}, {4, 4, 8, 16, 32, 32, 32}, {4, 4, 4, 8, 32, 32, 32},
+                                 {1, 1, 1, 1, 32, 32, 32}, {1, 1, 2, 1, 32, 32, 32}, {1, 1, 2, 4, 32, 32, 32}};
+    static const int Rs[6][7] = {{1, 1, 1, 1, 2, 4, 8}, {1, 2, 2, 2, 2, 4, 8}, {1, 2, 4, 4, 2, 4, 8},
+                                 {4, 8, 16, 32, 2, 4, 8}, {4, 8, 8, 32, 2, 4, 8}, {4, 8, 8, 8, 2, 4, 8}};
     *W = Ws[g_pack][cls];
     *R = Rs[g_pack][cls];
 }
@@ -1740,12 +1752,18 @@ static void launch_sim_impl(const SimArgs& a, int cls, int mode, int sm_count, c
             case 5: launch_sim_t<32, 4, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
             case 6: launch_sim_t<32, 8, MODE_DEEP>(a, sm_count, s, launches, grid_out); return;
         }
-    } else if (g_pack == 3 && cls <= 3) {
+    } else if (g_pack >= 3 && cls <= 3) {
         switch (cls) {
             case 0: launch_lane_t<1, 4>(a, sm_count, s, launches, grid_out); return;
             case 1: launch_lane_t<1, 8>(a, sm_count, s, launches, grid_out); return;
-            case 2: launch_lane_t<2, 8>(a, sm_count, s, launches, grid_out); return;
-            case 3: launch_lane_t<4, 8>(a, sm_count, s, launches, grid_out); return;
+            case 2:
+                if (g_pack == 3) launch_lane_t<1, 16>(a, sm_count, s, launches, grid_out);
+                else launch_lane_t<2, 8>(a, sm_count, s, launches, grid_out);
+                return;
+            case 3:
+                if (g_pack == 5) launch_lane_t<4, 8>(a, sm_count, s, launches, grid_out);
+                else launch_lane_t<1, 32>(a, sm_count, s, launches, grid_out);
+                return;
         }
     } else {
         switch (cls) {

@@ -108,7 +108,9 @@ class SweepStats(ctypes.Structure):
         "h2d_bytes", "d2h_bytes")] + [("num_ranks", ctypes.c_int32), ("gpu_launches", ctypes.c_int32)] + \
         [(n, ctypes.c_double) for n in ("ms_total", "ms_route", "ms_quality", "ms_rows", "ms_solve",
                                         "ms_k1", "k1_bytes", "ms_k4")] + [("collectives", ctypes.c_int64), ("quality_blocks", ctypes.c_int64),
-                                                           ("quality_blocks_seq", ctypes.c_int64)]
+                                                           ("quality_blocks_seq", ctypes.c_int64),
+                                                           ("waves_total", ctypes.c_int64), ("waves_run", ctypes.c_int64),
+                                                           ("plans_in_waves", ctypes.c_int64)]
 
 
 class SweepResultC(ctypes.Structure):

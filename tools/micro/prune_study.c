@@ -38,6 +38,30 @@ static int64_t run_rule(rowctx* x, int dp, double U, int K, int every, int rule,
             double amin = INFINITY;
             for (int j = 0; j < dp; ++j) amin = x->avail[j] < amin ? x->avail[j] : amin;
             int fut = 0;
+            if (rule == 2) {
+                /* K4 today: the exact count rounded down to blocks of 32 in output
+                   rank order, and k rounded up to a multiple of 32 */
+                int cex = 0;
+                for (int64_t j = 0; j < n; ++j) {
+                    double svc = INFINITY;
+                    for (int r = 0; r < dp; ++r) {
+                        const int s = x->rep_shape[r];
+                        const double v = x->prefill[s] + x->outs[j] * x->decode[s];
+                        svc = v < svc ? v : svc;
+                    }
+                    if (svc * (1.0 - 1e-12) - 1e-12 * x->arr[n - 1] > U) ++cex;
+                }
+                const int c32 = cex / 32 * 32;
+                /* requests of output rank < c32 arriving at j >= 32*ceil(k/32):
+                   rank by output descending, ties by index */
+                const int64_t k32 = (k + 31) / 32 * 32;
+                for (int64_t j = k32; j < n; ++j) {
+                    int rank = 0;
+                    for (int64_t i = 0; i < n; ++i)
+                        rank += (x->outs[i] > x->outs[j]) || (x->outs[i] == x->outs[j] && i < j);
+                    if (rank < c32) ++fut;
+                }
+            } else
             for (int64_t j = k; j < n; ++j) {
                 double svc = INFINITY;
                 for (int r = 0; r < dp; ++r) {
@@ -115,7 +139,7 @@ static void study_rec(studyctx* c, int idx, int* counts, int used) {
         const double U = c->U[used];
         int fa = 0, fb = 0;
         int64_t a = run_rule(x, dp, U, c->K, c->every, 0, &fa);
-        int64_t b = run_rule(x, dp, U, c->K, c->every, 1, &fb);
+        int64_t b = run_rule(x, dp, U, c->K, c->every, 2, &fb);
         if (a < 0) c->st->steps_full += -a; else { c->st->steps_a += a; c->st->pruned_a++; c->st->first_a += fa; }
         {
             int64_t kk = a < 0 ? -a : a;

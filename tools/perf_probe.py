@@ -11,6 +11,9 @@ parts = [eng.generate_trace(s, seed) for s, seed in W.trace_specs(name, count)]
 t = eng.concat_traces(parts) if len(parts) > 1 else parts[0]
 cfg, N = W.planner_config(name, t["scores"])
 E = eng.Engine(0)
+for kv in filter(None, os.environ.get("CG_OPTS", "").split(",")):  # e.g. CG_OPTS=k4_pack=4,pilot=0
+    k, v = kv.split("=")
+    E.set_option(k, int(v))
 for prune in prunes:
     E.set_option("prune", prune)
     for rep in range(reps):
