@@ -1235,16 +1235,36 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
         // k == u (mod 4) on every running lane: steps come in (even, odd)
         // pairs; after the even step the pair registers shift and the pair
         // after next is prefetched
+        if constexpr (R >= 16) {
+            // one inlined step (these step bodies are large: instruction-cache
+            // footprint over select savings); the parity is warp-uniform
 #pragma unroll 1
-        for (int u = 0; u < UNROLL; u += 2) {
-            step(tq.x, oq.x, tq.y);
-            const double t1 = tq.y, o1 = oq.y, tn1 = tq2.x;  // tn1: the next request's arrival
-            tq = tq2;
-            oq = oq2;
-            const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
-            tq2 = *reinterpret_cast<const double2*>(Trow + kp);
-            oq2 = *reinterpret_cast<const double2*>(Orow + kp);
-            step(t1, o1, tn1);
+            for (int u = 0; u < UNROLL; ++u) {
+                const bool odd = (u & 1) != 0;
+                const double t = odd ? tq.y : tq.x;
+                const double o = odd ? oq.y : oq.x;
+                const double tn1 = odd ? tq2.x : tq.y;  // the next request's arrival
+                if (odd) {
+                    tq = tq2;
+                    oq = oq2;
+                    const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
+                    tq2 = *reinterpret_cast<const double2*>(Trow + kp);
+                    oq2 = *reinterpret_cast<const double2*>(Orow + kp);
+                }
+                step(t, o, tn1);
+            }
+        } else {
+#pragma unroll 1
+            for (int u = 0; u < UNROLL; u += 2) {
+                step(tq.x, oq.x, tq.y);
+                const double t1 = tq.y, o1 = oq.y, tn1 = tq2.x;  // tn1: the next request's arrival
+                tq = tq2;
+                oq = oq2;
+                const int kp = (status == ST_RUN && k + 3 < n_req) ? k + 3 : 0;
+                tq2 = *reinterpret_cast<const double2*>(Trow + kp);
+                oq2 = *reinterpret_cast<const double2*>(Orow + kp);
+                step(t1, o1, tn1);
+            }
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
