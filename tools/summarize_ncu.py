@@ -7,6 +7,7 @@
 import csv
 import io
 import json
+import math
 import subprocess
 import sys
 
@@ -66,15 +67,27 @@ def launches(path):
 
 
 def k4_summary(path, source):
-    """Issue / warps-active utilisation of the captured K4 launches, weighted by duration."""
-    ks = report(path)
+    """Issue / warps-active utilisation of the captured K4 launches, weighted by
+    duration.  `path` is an .ncu-rep or the per-kernel JSON this tool wrote for
+    one; launches whose counters ncu left unset (nan) are skipped and counted."""
+    if path.endswith(".json"):
+        with open(path) as f:
+            ks = json.load(f)
+    else:
+        ks = report(path)
     tw = iw = ww = 0.0
+    skipped = 0
     for k in ks:
         t = float(k["gpu__time_duration.sum"].split()[0].replace(",", ""))
+        ia = float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])
+        wa = float(k["sm__warps_active.avg.pct_of_peak_sustained_active"].split()[0])
+        if not (math.isfinite(ia) and math.isfinite(wa)):
+            skipped += 1
+            continue
         tw += t
-        iw += t * float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"].split()[0])
-        ww += t * float(k["sm__warps_active.avg.pct_of_peak_sustained_active"].split()[0])
-    return {"source": source, "kernels_captured": len(ks),
+        iw += t * ia
+        ww += t * wa
+    return {"source": source, "kernels_captured": len(ks), "kernels_without_counters": skipped,
             "issue_active_pct_time_weighted": round(iw / tw, 2) if tw else None,
             "warps_active_pct_time_weighted": round(ww / tw, 2) if tw else None}
 
