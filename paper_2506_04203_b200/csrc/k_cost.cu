@@ -786,10 +786,17 @@ struct LaneTraits {
     // queues overflow to the DEEP re-run; 2-warp blocks pack shared memory
     static constexpr int CAP = R <= 4 ? 32 : (R <= 8 ? (W == 1 ? 8 : 16) : 4);
     static constexpr int WPB = R >= 16 ? 2 : 4;  // warps per block
+    // SA (R = 32): replica finish times in shared memory -- the idle mask is a
+    // fully unrolled scan of loads and compares, the winner's update one store
+    // (in registers it is a compare and two selects per replica per step) --
+    // and prefill/decode per part of the plan (<= kGsParts) so the footprint
+    // still fits two 2-warp blocks per SM
+    static constexpr bool SA = W == 1 && R >= 32;
+    static constexpr int PD = SA ? kGsParts : R;  // prefill/decode slots per lane
     static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
     // prefill, decode, head-job finish, previous-job finish (per replica slot)
-    static constexpr size_t pd_bytes = (size_t)4 * R * 32 * sizeof(double);
+    static constexpr size_t pd_bytes = (size_t)(2 * PD + (SA ? 3 : 2) * R) * 32 * sizeof(double);
     static constexpr size_t ht_bytes = (size_t)R * 32 * sizeof(unsigned);  // ring head | tail << 16
     static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
     static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + ht_bytes + hist_bytes + G * sizeof(GroupShared);
@@ -915,14 +922,17 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     unsigned char* wbase = smem + (size_t)warp * TR::bytes_per_warp;
     unsigned short* ring = reinterpret_cast<unsigned short*>(wbase);
     double* pre_s = reinterpret_cast<double*>(wbase + TR::ring_bytes);
-    double* dec_s = pre_s + R * 32;
-    double* nd_s = dec_s + R * 32;  // finish time of each replica's head job (INF: none)
+    constexpr int PD = TR::PD;
+    constexpr bool SA = TR::SA;
+    double* dec_s = pre_s + PD * 32;
+    double* nd_s = dec_s + PD * 32;  // finish time of each replica's head job (INF: none)
     // finish of the job before each replica's last one (INF: no replica; a
     // value <= t means the replica holds exactly one job at t).  Only the
     // winner's slot changes per step, so prev and the ring heads live in
     // shared memory (one predicated store) rather than in registers (a
     // select per replica per step).
     double* prev_s = nd_s + R * 32;
+    double* avail_s = prev_s + R * 32;  // SA: finish of each replica's last job
     unsigned* ht_s = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
     unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes);
     GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes +
@@ -953,14 +963,33 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     // per replica: avail = finish of its last job (registers: every step's
     // idle mask reads them all); the head job's finish (nd_s), the previous
     // job's finish (prev_s) and the ring head/tail (ht_s) live in shared memory
-    double avail[R];
+    double avail[SA ? 1 : R];
+    // finish of replica r's last job
+    auto av_get = [&](int r) -> double {
+        if constexpr (SA) return avail_s[r * 32 + lane];
+        else return avail[r];
+    };
+    auto av_set = [&](int r, double v) {
+        if constexpr (SA) avail_s[r * 32 + lane] = v;
+        else avail[r] = v;
+    };
+    unsigned pstart = 0;  // SA: bit r set when replica r starts a new part
+    // shared-memory slot of replica r's prefill/decode
+    auto pd_slot = [&](int r) -> int {
+        if constexpr (SA) {
+            const int q = __popc(pstart & ((2u << r) - 1u)) - 1;
+            return (q > 0 ? q : 0) * 32 + lane;
+        } else {
+            return r * 32 + lane;
+        }
+    };
     // W == 1: output tokens of the job at the ring head, loaded one pop ahead
     // (the lanes' rows differ, so a load at pop time would stall on L2)
     constexpr bool HO = W == 1 && R <= 8;
     double ho[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        avail[r] = INF;
+        av_set(r, INF);
         ho[r] = 0.0;
         ht_s[r * 32 + lane] = 0u;
         prev_s[r * 32 + lane] = INF;
@@ -992,11 +1021,19 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             __syncwarp();
             if (need) {
                 status = gs.status;
+                if (SA && status == ST_RUN && gs.nparts == 0) {
+                    // more parts than the per-part tables hold: the DEEP re-run takes it
+                    const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
+                    if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)gs.row << kItemPlanBits) | gs.plan;
+                    status = ST_NEED;
+                    gs.status = ST_NEED;
+                }
                 if (status == ST_RUN) {
                     row = gs.row;
                     dp = gs.dp;
                     gpus = gs.used;
                     plan = gs.plan;
+                    pstart = 0u;
                     const long long rb = (long long)row * kMaxShapes;
                     Trow = a.tab.T + (long long)row * a.tab.ld;
                     Orow = a.tab.O + (long long)row * a.tab.ld;
@@ -1008,13 +1045,18 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                         const int j = gl * R + r;
                         nd_s[r * 32 + lane] = INF;
                         ht_s[r * 32 + lane] = 0u;
-                        avail[r] = INF;
+                        av_set(r, INF);
                         prev_s[r * 32 + lane] = INF;
                         if (j < dp) {
                             if (np > 0) {
                                 while (j >= cum) {
                                     sh = gs.pshape[q];
                                     cum += gs.pcount[q];
+                                    if (SA) {
+                                        pre_s[q * 32 + lane] = a.tab.prefill[rb + sh];
+                                        dec_s[q * 32 + lane] = a.tab.decode[rb + sh];
+                                        pstart |= 1u << r;
+                                    }
                                     ++q;
                                 }
                             } else {
@@ -1023,9 +1065,11 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                                     cum += gs.counts[sh];
                                 }
                             }
-                            pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
-                            dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
-                            avail[r] = 0.0;
+                            if (!SA) {
+                                pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
+                                dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
+                            }
+                            av_set(r, 0.0);
                             prev_s[r * 32 + lane] = 0.0;
                         }
                     }
@@ -1063,7 +1107,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             // time is known
             unsigned mn = 0;
 #pragma unroll
-            for (int r = 0; r < R; ++r) mn |= (avail[r] <= tn1) ? (1u << r) : 0u;
+            for (int r = 0; r < R; ++r) mn |= (av_get(r) <= tn1) ? (1u << r) : 0u;
             // a sojourn counts toward the prune test only while the FIFOs are
             // intact (no ring overflow in the group so far)
             const bool intact = W == 1 ? !ovf : ((__ballot_sync(FULL, ovf) >> gshift) & wmask) == 0u;
@@ -1081,7 +1125,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             int rr = __ffs(m) - 1;
             // the idle candidate's finish (start = t), issued before the busy
             // block so its shared-memory loads and fp64 chain overlap it
-            const int pidx0 = (rr > 0 ? rr : 0) * 32 + lane;
+            const int pidx0 = pd_slot(rr > 0 ? rr : 0);
             double fin = __dadd_rn(__dadd_rn(t, pre_s[pidx0]), __dmul_rn(o, dec_s[pidx0]));
             double start = t;
             unsigned H = 0;
@@ -1116,7 +1160,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                         for (int r = 0; r < R; ++r) {
                             const bool lz = (lazy >> r) & 1u;
                             if (lz) {
-                                nd_s[r * 32 + lane] = avail[r];
+                                nd_s[r * 32 + lane] = av_get(r);
                                 const unsigned hr = ht_s[r * 32 + lane];
                                 ht_s[r * 32 + lane] = (hr & 0xffff0000u) | (hr >> 16);
                             }
@@ -1138,8 +1182,8 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                             if (HO) oh = ho[r];
                             else if (more) oh = Orow[ring[(r * CAP + (int)(h & (CAP - 1))) * 32 + lane]];
                             const double ndr = nd_s[r * 32 + lane];
-                            const double nx = __dadd_rn(__dadd_rn(ndr, pre_s[r * 32 + lane]),
-                                                        __dmul_rn(oh, dec_s[r * 32 + lane]));
+                            const int pr = pd_slot(r);
+                            const double nx = __dadd_rn(__dadd_rn(ndr, pre_s[pr]), __dmul_rn(oh, dec_s[pr]));
                             const double nn = more ? nx : INF;
                             nd_s[r * 32 + lane] = nn;
                             const unsigned h1 = (h + 1u) & 0xffffu;
@@ -1175,18 +1219,22 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 }
                 if (busy) {
                     // avail of replica rr: select tree on rr's bits; its ring state from shared memory
-                    double av[R];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) av[r] = avail[r];
-#pragma unroll
-                    for (int w = 1; w < R; w <<= 1) {
-                        const bool hi = (rr & w) != 0;
-#pragma unroll
-                        for (int r = 0; r + w < R; r += 2 * w) av[r] = hi ? av[r + w] : av[r];
-                    }
                     H = ht_s[rr * 32 + lane];
-                    start = av[0];  // > t: std::max(t, avail)
-                    const int pidx = rr * 32 + lane;
+                    if constexpr (SA) {
+                        start = avail_s[rr * 32 + lane];  // > t: std::max(t, avail)
+                    } else {
+                        double av[R];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) av[r] = av_get(r);
+#pragma unroll
+                        for (int w = 1; w < R; w <<= 1) {
+                            const bool hi = (rr & w) != 0;
+#pragma unroll
+                            for (int r = 0; r + w < R; r += 2 * w) av[r] = hi ? av[r + w] : av[r];
+                        }
+                        start = av[0];  // > t: std::max(t, avail)
+                    }
+                    const int pidx = pd_slot(rr);
                     fin = __dadd_rn(__dadd_rn(start, pre_s[pidx]), __dmul_rn(o, dec_s[pidx]));
                 }
             }
@@ -1214,8 +1262,12 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     prev_s[rr * 32 + lane] = start;
                     ht_s[rr * 32 + lane] = H;
                 }
+                if constexpr (SA) {
+                    if (me) avail_s[rr * 32 + lane] = fin;
+                } else {
 #pragma unroll
-                for (int r = 0; r < R; ++r) avail[r] = (me && r == rr) ? fin : avail[r];
+                    for (int r = 0; r < R; ++r) avail[r] = (me && r == rr) ? fin : avail[r];
+                }
                 if (HO && first) {  // the job is the head of an empty ring (rarer than a step)
 #pragma unroll
                     for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
