@@ -51,7 +51,8 @@ struct RowTables {
     double* prefill;
     double* decode;
     double* mean_service;
-    double* inv_service;  // fl(1 / mean_service): the filter's fast stability test
+    double* inv_service;  // fl(1 / mean_service), NaN for infeasible shapes: the filter's fast stability test
+    double* svc_k;        // prefill + o_(K) * decode: the filter's per-part service bound term
     double* T;            // [row][ld] CRN arrivals (first n_req used)
     double* O;            // [row][ld] CRN outputs
     int ld;               // row stride: n_req rounded up to a multiple of 4 (32-byte rows)

@@ -238,6 +238,7 @@ void class_shape(int cls, int* W, int* R);
 void class_dp_range(int cls, int* lo, int* hi);
 SimGeometry sim_geometry(int cls, int mode, int sm_count);
 void launch_row_setup(const RowSetupArgs& a, const double* L, cudaStream_t s, int* launches);
+void launch_row_svck(const RowTables& tab, int nrows, int kstar, cudaStream_t s, int* launches);
 void launch_plan_filter(const FilterArgs& a, cudaStream_t s, int* launches);
 void launch_sim(const SimArgs& a, int cls, int mode, int sm_count, cudaStream_t s, int* launches,
                 int* grid_out);

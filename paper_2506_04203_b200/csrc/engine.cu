@@ -214,7 +214,7 @@ struct cg_engine {
     DevBuf d_gvals, d_ranks, d_hist, d_flags, d_lk0, d_lv0, d_lk1, d_lv1, d_rshist, d_orax;
     DevBuf d_p95tab;
     DevBuf d_wcount, d_wsin, d_wsout, d_wsinf, d_wsoutf, d_wp95i, d_wp95o, d_wstats, d_thr, d_qsum, d_qa, d_qe, d_qu, d_qseq;
-    DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_ims, d_T, d_O, d_crn;
+    DevBuf d_rows, d_spaces, d_ways, d_models, d_ok, d_pre, d_dec, d_ms, d_ims, d_svck, d_T, d_O, d_crn;
     DevBuf d_latmin, d_ub, d_ties, d_tiecnt, d_ovf, d_ovfcnt, d_ovfcnt2, d_rowids, d_iprefix, d_ictr,
         d_scratch, d_ring, d_seeds, d_partials, d_lists, d_lkeys, d_lcount, d_tpart, d_ctrs, d_best, d_flat, d_fplan, d_gather, d_send;
     DevBuf d_wlrow, d_tfeas, d_tL, d_talloc, d_tplan, d_g2d, d_ctuple, d_cflag, d_pos, d_total, d_ecand,
@@ -337,6 +337,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     tab.decode = E.d_dec.as<double>((size_t)nrows * kMaxShapes);
     tab.mean_service = E.d_ms.as<double>((size_t)nrows * kMaxShapes);
     tab.inv_service = E.d_ims.as<double>((size_t)nrows * kMaxShapes);
+    tab.svc_k = E.d_svck.as<double>((size_t)nrows * kMaxShapes);
     tab.ld = (n_req + 3) & ~3;
     const std::vector<double> L = crn_log1p_table(q.queueing_sim_seed, n_req);  // glibc log1p (H3), once
     {
@@ -426,6 +427,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
         kstar = idx[K - 1];
     }
+    launch_row_svck(tab, nrows, kstar, x.s, &x.launches);
     // rows with a non-empty plan space
     std::vector<int> prow;
     std::vector<unsigned long long> chunk_prefix(1, 0);

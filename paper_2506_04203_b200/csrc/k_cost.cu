@@ -83,7 +83,8 @@ __global__ void k_row_shapes(RowSetupArgs a) {
     const bool ok = dev_memory_feasible(tp, pp, m, a.hw, a.p, kv_tokens);
     a.tab.shape_ok[o] = ok ? 1 : 0;
     if (!ok) {
-        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = a.tab.inv_service[o] = 0.0;
+        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = 0.0;
+        a.tab.inv_service[o] = __longlong_as_double(0x7ff8000000000000ll);  // any plan using it is unstable
         return;
     }
     // service_time (costmodel.cpp:176-194) with the reference's op order
@@ -1562,20 +1563,17 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
             // cnt * fl(1/ms) is within 2u(1+u) of cnt/ms and both sums carry at
             // most S roundings, so the two capacities differ by < 2(S+3)u <
             // 1e-13 relative; only rates inside that band take the exact path.
-            bool good = true;
+            // an infeasible shape has inv_service NaN: the capacity is NaN and
+            // both stability tests below fail, as the reference's `ok` does
             double capacity = 0.0, lb = __longlong_as_double(0x7ff0000000000000ll), slow = 0.0;
             for (unsigned m = nz; m; m &= m - 1u) {
                 const int s = __ffs(m) - 1;
-                const int cnt = c[s];
-                if (!a.tab.shape_ok[rb + s]) {
-                    good = false;
-                    break;
-                }
-                capacity += (double)cnt * a.tab.inv_service[rb + s];
-                const double v = a.tab.prefill[rb + s] + o_k * a.tab.decode[rb + s];
+                capacity += (double)c[s] * a.tab.inv_service[rb + s];
+                const double v = a.tab.svc_k[rb + s];  // prefill + o_(K) decode
                 lb = v < lb ? v : lb;
                 slow = v > slow ? v : slow;
             }
+            const bool good = capacity == capacity;
             bool stable_plan = good && rd.rate < capacity * (1.0 - 1e-13);
             if (good && !stable_plan && rd.rate < capacity * (1.0 + 1e-13)) {  // the exact reference sum
                 double exact = 0.0;
@@ -1595,11 +1593,15 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 // order heuristics (results never depend on them): 1 fast-shape
                 // bound / (1 - rho), 3 (default) mean of the fastest and slowest
                 // shapes' bounds / (1 - rho), ...
-                const double rho = rd.rate / capacity;
+                // (order only: the default key is computed in float)
                 double est = lb;
+                if (a.sort_key == 3) {
+                    const float rho = __fdividef((float)rd.rate, (float)capacity);
+                    est = (double)__fdividef(0.5f * ((float)lb + (float)slow), 1.0f - rho);
+                }
+                const double rho = a.sort_key == 3 ? 0.0 : rd.rate / capacity;
                 if (a.sort_key == 1) est = lb / (1.0 - rho);
                 else if (a.sort_key == 2) est = lb / ((1.0 - rho) * (1.0 - rho));
-                else if (a.sort_key == 3) est = 0.5 * (lb + slow) / (1.0 - rho);
                 else if (a.sort_key == 4) est = slow / (1.0 - rho);
                 else if (a.sort_key == 5) est = 0.25 * (lb + 3.0 * slow) / (1.0 - rho);
                 else if (a.sort_key == 6) est = slow / ((1.0 - rho) * (1.0 - rho));
@@ -1880,6 +1882,24 @@ void launch_pilot_lists(const PilotArgs& a, cudaStream_t s, int* launches) {
 void launch_plan_filter(const FilterArgs& a, cudaStream_t s, int* launches) {
     if (a.nchunks == 0) return;
     k_plan_filter<<<(unsigned)((a.nchunks + 127) / 128), 128, 0, s>>>(a);
+    CG_LAUNCH_CHECK();
+    if (launches) ++*launches;
+}
+
+// The filter's per-(row, shape) service term prefill + o_(K) decode (o_(K):
+// the K-th largest CRN output, the same request index for every row).
+__global__ void k_row_svck(RowTables tab, int nrows, int kstar) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= (long long)nrows * kMaxShapes) return;
+    const long long row = t / kMaxShapes;
+    const double o_k = tab.O[row * tab.ld + kstar];
+    tab.svc_k[t] = tab.prefill[t] + o_k * tab.decode[t];
+}
+
+void launch_row_svck(const RowTables& tab, int nrows, int kstar, cudaStream_t s, int* launches) {
+    if (nrows == 0) return;
+    const long long work = (long long)nrows * kMaxShapes;
+    k_row_svck<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(tab, nrows, kstar);
     CG_LAUNCH_CHECK();
     if (launches) ++*launches;
 }
