@@ -251,13 +251,15 @@ void* cg_engine_stream(cg_engine* engine);
  *   "k4_pack"          3 (default) lane-major k_lane for dp <= 32, one lane per plan (R = 4/8/16/32
  *                      replicas per lane); 4: W = 1/1/2/1 lanes per plan, R = 4/8/8/32; 5: W = 1/1/2/4,
  *                      R = 4/8/8/8; 0-2 group-per-plan k_sim forms
- *   "pilot"            1 (default) best-estimate plan per (row, budget) simulated first
+ *   "pilot"            best-estimate plan per (row, budget) simulated first: 1 (default) when the
+ *                      sweep's plan lists fit one filter wave, 2 always, 0 never
  *   "pilot_merge"      1 (default) pilot launch grouping (0 per class, 2 one launch)
  *   "pilot_min_plans"  0 (default) rows with fewer plans get no pilot
  *   "pilot_sort"       1 (default) pilot lists in ascending estimate order
  *   "sort_key"         3 (default) work-list order estimate (0 raw service bound)
  *   "class_order"      1 (default) replica-count classes ascending (0 descending)
- *   "wave_plans"       64 (default) plans per filter wave in units of 2^20 (~248 B of HBM per plan)
+ *   "wave_plans"       256 (default) plans per filter wave in units of 2^20; class lists sized by a
+ *                      census of the plan spaces, the wave shrunk to fit 60% of the free HBM
  *   "conc_lists_max"   65536 (default) waves with at most this many listed plans run their
  *                      replica-count classes concurrently on four streams (0: never)
  *   "quality_form"     1 (default) block-parallel exact K2 quality sums; 0 one fp64 add chain per tuple

@@ -205,7 +205,7 @@ struct FilterArgs {
     ItemRec* recs[7];                          // listed plans (ItemRec)
     unsigned long long* keys[7];               // coarse service-bound order keys
     unsigned long long* list_count;            // [7]
-    unsigned long long list_cap;               // per class
+    unsigned long long list_caps[7];           // per class
     unsigned long long* counters;
     unsigned long long* pilot;                 // optional [row][N+1]: (estimate20 << 44 | plan) minimum
     int pilot_only;                            // 1: only the pilot minima (no lists, no counters)

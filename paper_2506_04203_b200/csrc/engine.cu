@@ -190,14 +190,14 @@ struct cg_engine {
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
-    int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot)
+    int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
     int pilot_sort = 1;             // pilot lists in ascending estimate order (option pilot_sort)
     int sort_key = 3;   // list/pilot order (option sort_key): 0 service bound, else an estimate (k_plan_filter)
     int class_order = 1;  // 0: lists by replica count descending, 1: ascending (option class_order)
     long long conc_lists_max = 1 << 16;  // waves with at most this many listed plans run classes concurrently
-    int wave_plans = 64;  // plans per filter wave, in units of 2^20 (option wave_plans; ~248 B of lists per plan)
+    int wave_plans = 256;  // plans per filter wave, in units of 2^20 (option wave_plans; <= 60% of free HBM)
     int k4_pack = 3;  // lane packing of the JSQ kernel classes (see class_shape; 3 = lane-major k_lane)
     int quality_form = 1;  // K2: 1 block-parallel exact (binade units), 0 one fp64 chain per tuple
     int quality_block = 0; // K2: minimum requests per block (diagnostic; 0 = automatic)
@@ -548,7 +548,52 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     // re-visited by the filtered lists (idempotent), so this only moves work.
     // With the pilot pass on, the seeds run in the pilot launch instead.
     std::vector<unsigned long long> seeds;
-    const bool use_pilot = E.pilot && E.prune && !prow.empty();
+    // this rank's chunks: global chunk g belongs to rank g mod world (local
+    // chunk l = global l*world + rank); every rank runs the same number of
+    // waves (the largest share's), so the per-wave bound exchanges pair up
+    const unsigned long long my_chunks = shard_count(chunk_prefix.back(), E.rank, E.world);
+    const unsigned long long max_chunks = shard_count(chunk_prefix.back(), 0, E.world);
+    // wave capacity: wave_plans, never more than this rank's plans, and the
+    // class lists of a wave within 60% of the free device memory
+    unsigned long long wave_chunks = std::max<unsigned long long>(
+        1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk, max_chunks));
+    // per-class list capacity: one wave, but never more plans than the sweep's
+    // rows hold in that replica-count class (a host census of the plan spaces)
+    unsigned long long class_total[7] = {0, 0, 0, 0, 0, 0, 0};
+    {
+        std::vector<std::array<unsigned long long, 7>> per_space(hs.size());
+        std::vector<char> done(hs.size(), 0);
+        for (int r : prow) {
+            const int sp = rows[r].space;
+            if (!done[sp]) {
+                hs[sp].class_counts(per_space[sp].data());
+                done[sp] = 1;
+            }
+            for (int c = 0; c < 7; ++c) class_total[c] += per_space[sp][c];
+        }
+    }
+    unsigned long long ccap[7], coff[8], cmax = 1;
+    auto size_lists = [&]() {
+        coff[0] = 0;
+        cmax = 1;
+        for (int c = 0; c < 7; ++c) {
+            ccap[c] = std::min<unsigned long long>(wave_chunks * chunk, class_total[c]);
+            coff[c + 1] = coff[c] + ccap[c];
+            cmax = std::max(cmax, ccap[c]);
+        }
+        // recs + keys per listed slot; sort / gather temporaries per class
+        return (double)coff[7] * (sizeof(ItemRec) + 8) + (double)cmax * (sizeof(ItemRec) + 40);
+    };
+    {
+        size_t fr = 0, tot = 0;
+        const double budget = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? 0.6 * (double)fr : 64e9;
+        while (size_lists() > budget && wave_chunks > 1) wave_chunks = (wave_chunks + 1) / 2;
+    }
+    const unsigned long long nwaves = (max_chunks + wave_chunks - 1) / wave_chunks;
+    // pilot pass (option pilot): 1 = automatic -- single-wave sweeps only (a
+    // multi-wave sweep's first sorted wave seeds the bounds as well, without a
+    // second enumeration of every plan); 2 = always; 0 = never
+    const bool use_pilot = E.prune && !prow.empty() && (E.pilot == 2 || (E.pilot == 1 && nwaves <= 1));
     const bool collective = E.collective();
     // Ranks share their bounds: one all-gather of ub and a min over ranks
     // (every rank's ub is realised by one of its own plans, so the min is a
@@ -591,22 +636,13 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned long long* cpre = E.d_iprefix.as<unsigned long long>(chunk_prefix.size());
         x.h2d(rowids, prow.data(), prow.size() * sizeof(int));
         x.h2d(cpre, chunk_prefix.data(), chunk_prefix.size() * 8);
-        // this rank's chunks: global chunk g belongs to rank g mod world
-        // (local chunk l = global l*world + rank); every rank runs the same
-        // number of waves (the largest share's), so the per-wave bound
-        // exchanges pair up
-        const unsigned long long my_chunks = shard_count(chunk_prefix.back(), E.rank, E.world);
-        const unsigned long long max_chunks = shard_count(chunk_prefix.back(), 0, E.world);
-        // list capacity: one wave, but never more than this rank's plans
-        const unsigned long long wave_chunks = std::max<unsigned long long>(
-            1, std::min<unsigned long long>(((unsigned long long)E.wave_plans << 20) / chunk, max_chunks));
-        const unsigned long long cap = wave_chunks * chunk;
-        ItemRec* lrecs = E.d_lrecs.as<ItemRec>((size_t)7 * cap);
-        unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cap);
-        unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)7 * cap);
-        unsigned long long* tk = E.d_lk1.as<unsigned long long>(cap);
-        unsigned long long* tv = E.d_lv1.as<unsigned long long>(cap);
-        unsigned int* rsh = E.d_rshist.as<unsigned int>(radix_hist_entries((long long)cap));
+        size_lists();
+        ItemRec* lrecs = E.d_lrecs.as<ItemRec>((size_t)coff[7]);
+        unsigned long long* tidx = E.d_lidx.as<unsigned long long>(cmax);
+        unsigned long long* lkeys = E.d_lkeys.as<unsigned long long>((size_t)coff[7]);
+        unsigned long long* tk = E.d_lk1.as<unsigned long long>(cmax);
+        unsigned long long* tv = E.d_lv1.as<unsigned long long>(cmax);
+        unsigned int* rsh = E.d_rshist.as<unsigned int>(radix_hist_entries((long long)cmax));
         unsigned long long* lcount = E.d_lcount.as<unsigned long long>(7);
         // pilot: the best-estimate stable plan of every (row, budget) cell
         const size_t pregion = (size_t)cells + seeds.size();  // per-class pilot list capacity
@@ -729,17 +765,19 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             fa.tab = tab;
             fa.ub = ub;
             for (int c = 0; c < 7; ++c) {
-                fa.recs[c] = lrecs + (size_t)c * cap;
-                fa.keys[c] = lkeys + (size_t)c * cap;
+                fa.recs[c] = lrecs + coff[c];
+                fa.keys[c] = lkeys + coff[c];
+                fa.list_caps[c] = ccap[c];
             }
             fa.list_count = lcount;
-            fa.list_cap = cap;
             fa.counters = ctrs;
             fa.sort_key = E.sort_key;
             launch_plan_filter(fa, x.s, &x.launches);
             unsigned long long counts[7];
             x.d2h(counts, lcount, sizeof(counts));
             x.sync();
+            for (int c = 0; c < 7; ++c)  // the census bounds every class list: cannot happen
+                if (counts[c] > ccap[c]) fail(CG_ERR_CUDA, "plan class list overflow");
             if (pilot_join) {
                 CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[11], 0));
                 pilot_join = false;
@@ -758,13 +796,13 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             if (conc) CG_CUDA(cudaEventRecord(E.ev[12], x.s));  // re-recorded after the sorts below
             for (int ci = 0; ci < 7; ++ci) {
                 const int c = E.class_order ? ci : 6 - ci;
-                const ItemRec* recs = lrecs + (size_t)c * cap;
+                const ItemRec* recs = lrecs + coff[c];
                 const unsigned long long* perm = nullptr;
                 if (E.prune && counts[c] > 1) {  // ascending order key (16 bits: 2 passes) of slot indices
                     k_iota_u64<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(tidx, (long long)counts[c]);
                     CG_LAUNCH_CHECK();
                     ++x.launches;
-                    const int par = radix_sort_u64(lkeys + (size_t)c * cap, tidx, tk, tv, (long long)counts[c],
+                    const int par = radix_sort_u64(lkeys + coff[c], tidx, tk, tv, (long long)counts[c],
                                                    (1ull << kListKeyBits) - 1ull, rsh, x.s, &x.launches);
                     perm = par ? tv : tidx;
                     if (conc) {  // the shared sort buffers are reused by the next class
@@ -776,7 +814,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
                 if (!conc) {
                     const ItemRec* lr = recs;
                     if (perm) {  // gather into sorted order (the class lists run one after another)
-                        ItemRec* gr = E.d_grecs.as<ItemRec>(cap);
+                        ItemRec* gr = E.d_grecs.as<ItemRec>(cmax);
                         k_gather_recs<<<(unsigned)((counts[c] + 255) / 256), 256, 0, x.s>>>(
                             perm, (long long)counts[c], lr, gr);
                         CG_LAUNCH_CHECK();
@@ -1925,7 +1963,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
-        else if (k == "pilot") e->pilot = (int)value;
+        else if (k == "pilot") e->pilot = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "class_order") e->class_order = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);

@@ -145,6 +145,25 @@ struct HostPlanSpace {
             if (min_gpus == 0 || sh.gpus < min_gpus) min_gpus = sh.gpus;
     }
 
+    // Number of plans in each replica-count class (dp <= 4, 8, 16, 32, 64,
+    // 128, 255): knapsack over (GPUs, replicas), the empty plan excluded.
+    void class_counts(unsigned long long out[7]) const {
+        for (int c = 0; c < 7; ++c) out[c] = 0;
+        const int D = 256;
+        std::vector<unsigned long long> f((size_t)(N + 1) * D, 0ull);
+        f[0] = 1;
+        for (const auto& sh : shapes)
+            for (int b = sh.gpus; b <= N; ++b)
+                for (int d = 1; d < D; ++d) f[(size_t)b * D + d] += f[(size_t)(b - sh.gpus) * D + d - 1];
+        static const int His[7] = {4, 8, 16, 32, 64, 128, 255};
+        for (int b = 1; b <= N; ++b)
+            for (int d = 1; d < D; ++d) {
+                int c = 0;
+                while (c < 6 && d > His[c]) ++c;
+                out[c] += f[(size_t)b * D + d];
+            }
+    }
+
     // plan index -> counts (mirror of the device unrank)
     void unrank(unsigned long long p, std::vector<int>& c) const {
         const int S = (int)shapes.size();

@@ -1636,7 +1636,7 @@ __global__ void __launch_bounds__(128) k_plan_filter(FilterArgs a) {
                 if (lane == leader) base = atomicAdd(&a.list_count[cls], (unsigned long long)__popc(peers));
                 base = __shfl_sync(peers, base, leader);
                 const unsigned long long slot = base + __popc(peers & ((1u << lane) - 1u));
-                if (slot < a.list_cap) {
+                if (slot < a.list_caps[cls]) {
                     ItemRec r;
                     r.item = ((unsigned long long)row << kItemPlanBits) | p;
                     encode_rec(r, c, sp.S, used);
