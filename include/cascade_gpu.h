@@ -266,6 +266,7 @@ void* cg_engine_stream(cg_engine* engine);
  *   "p95_tables"       1 (default) K3 chunk tables for traces >= 65536 requests; 0 direct column scans
  *   "max_waves", "wave_stride"  rate sampling only: run at most max_waves filter waves, every
  *                      wave_stride-th one; the result is then PARTIAL (stats.waves_run < waves_total)
+ *   "fut_block"        1 (default) output-rank granularity of K4's future-service bound (exact counts)
  *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle",
  *   "quality_block" (diagnostic)
  * Unknown keys return CG_ERR_INVALID_INPUT. */

@@ -62,7 +62,7 @@ struct RowTables {
     int nc;
     const int* probe_req; // [nc] request index of block i's smallest output
     double* Pv;           // [row][nc]
-    const unsigned* fut;  // [(nc+1)][nc]
+    const unsigned* fut;  // [(na+1)][nc], na = arrival blocks of 32
 };
 
 struct SimItem {

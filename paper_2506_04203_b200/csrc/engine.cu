@@ -190,6 +190,7 @@ struct cg_engine {
     int ub_oracle = 0;   // diagnostic: seed K4's bounds with the previous identical sweep's rows
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
+    int fut_block = 1;  // output-rank block of the future bound (option fut_block; 1 = exact counts)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
@@ -347,18 +348,22 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         for (int k = 0; k < n_req; ++k) desc[k] = k;
         std::stable_sort(desc.begin(), desc.end(), [&](int a, int b) { return L[2 * a + 1] < L[2 * b + 1]; });
         for (int k = 0; k < n_req; ++k) pos[desc[k]] = k;
-        const int nc = (n_req + 31) / 32;
+        // output ranks in blocks of RB requests (option fut_block; 1 = exact
+        // counts), arrivals in blocks of 32 (the prune checks' granularity)
+        const int RB = E.fut_block;
+        const int nc = (n_req + RB - 1) / RB;
+        const int na = (n_req + 31) / 32;
         std::vector<int> probe(nc);
-        for (int i = 0; i < nc; ++i) probe[i] = desc[std::min(32 * i + 31, n_req - 1)];
-        // fut[c][i] = #requests j >= 32c whose output rank block pos[j]/32 <= i,
+        for (int i = 0; i < nc; ++i) probe[i] = desc[std::min(RB * i + RB - 1, n_req - 1)];
+        // fut[c][i] = #requests j >= 32c whose output rank block pos[j]/RB <= i,
         // built backwards: fut[c] = fut[c+1] + the prefix histogram of block c
         std::vector<unsigned> fut;
         if (E.fut_bound) {
-            fut.assign((size_t)(nc + 1) * nc, 0u);
+            fut.assign((size_t)(na + 1) * nc, 0u);
             std::vector<unsigned> h(nc);
-            for (int c = nc - 1; c >= 0; --c) {
+            for (int c = na - 1; c >= 0; --c) {
                 std::fill(h.begin(), h.end(), 0u);
-                for (int j = 32 * c; j < std::min(32 * c + 32, n_req); ++j) ++h[pos[j] / 32];
+                for (int j = 32 * c; j < std::min(32 * c + 32, n_req); ++j) ++h[pos[j] / RB];
                 unsigned run = 0;
                 for (int i = 0; i < nc; ++i) {
                     run += h[i];
@@ -1963,6 +1968,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "ub_oracle") e->ub_oracle = (int)value;
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
+        else if (k == "fut_block") e->fut_block = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
         else if (k == "pilot") e->pilot = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "class_order") e->class_order = (int)value;
