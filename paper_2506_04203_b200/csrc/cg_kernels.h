@@ -149,6 +149,7 @@ struct SimArgs {
     int N, n_req, K, prune;
     int kstar;                                 // index of the K-th largest CRN output
     int check_stable;                          // 1: items are not pre-filtered (seeds)
+    unsigned lane_check;                       // k_lane: prune checks every 4(lane_check+1) request-steps
     int seeds;                                 // 1: count completions as seeding work
     const unsigned long long* items;           // packed (row, plan) work items (when recs == nullptr)
     const ItemRec* recs;                       // filtered items with parts and bound (else nullptr)

@@ -191,6 +191,7 @@ struct cg_engine {
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
     int fut_block = 1;  // output-rank block of the future bound (option fut_block; 1 = exact counts)
+    int lane_check = 32;  // k_lane request-steps between prune checks (option lane_check: 8, 16, 32, 64)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
@@ -479,6 +480,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     base.sld = sld;
     base.counters = ctrs;
     base.ring_cap = ring_cap;
+    base.lane_check = (unsigned)(E.lane_check / 4 - 1);  // k_lane runs 4 request-steps per trip
 
     // Runs one packed work list through the class kernel; ring overflows are
     // appended to the class's overflow region.
@@ -1969,6 +1971,10 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "fut_block") e->fut_block = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
+        else if (k == "lane_check") {
+            if (value != 8 && value != 16 && value != 32 && value != 64) fail(CG_ERR_INVALID_INPUT, "lane_check must be 8, 16, 32 or 64");
+            e->lane_check = (int)value;
+        }
         else if (k == "pilot") e->pilot = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
         else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "class_order") e->class_order = (int)value;

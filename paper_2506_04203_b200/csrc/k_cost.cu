@@ -904,7 +904,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
     return true;
 }
 
-constexpr unsigned kLaneCheck = 32;  // request-steps between exact-bound prune checks
+// request-steps between exact-bound prune checks: SimArgs::lane_check (engine option lane_check)
 
 template <int W, int R>
 __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::MIN_BLOCKS) k_lane(SimArgs a) {
@@ -1096,6 +1096,20 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
         U = __shfl_sync(FULL, U, gshift);  // one bound per group (leader's)
+
+        // a trip that ends with a prune check issues the check's loads now (the
+        // future-bound count at the trip's end step and the live bound), so their
+        // L2 latency overlaps the trip's steps; an earlier bound is a larger one,
+        // still valid (sojourns above it exceed every later bound as well)
+        const bool check_trip = (it & a.lane_check) == a.lane_check;
+        int fut_pre = 0;
+        double U_pre = U;
+        if (check_trip && status == ST_RUN) {
+            if (qi > 0) fut_pre = (int)a.tab.fut[(long long)((k + UNROLL + 31) >> 5) * a.tab.nc + (qi - 1)];
+            if (a.prune)
+                U_pre = __longlong_as_double(
+                    (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
+        }
 
         // ---- phase B: UNROLL request-steps per running plan, as pairs (rows
         // and k are even-aligned) with the next pair's arrivals/outputs
@@ -1321,7 +1335,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
         }
 
         // ---- phase C: periodic exact-bound pruning and overflow checks
-        if ((it & (kLaneCheck / UNROLL - 1u)) == (kLaneCheck / UNROLL - 1u)) {
+        if (check_trip) {
             int tot = ab;
             int ov = ovf ? 1 : 0;
 #pragma unroll
@@ -1333,7 +1347,10 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 // qi comes from the launch's bound snapshot (>= the live bound):
                 // sojourns counted against any of the bounds seen exceed the
                 // smallest of them, itself a latency found at <= gpus
-                const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
+                // fut_pre counts the plan's future requests from step k0 + UNROLL
+                // on (k0: k at the trip's start); k <= k0 + UNROLL here, so it
+                // counts only requests still to come
+                const int fut = fut_pre;
                 if (a.prune && tot + fut >= a.K) {  // tot: sojourns of intact steps only
                     pruned += 1;
                     steps += k;
@@ -1346,8 +1363,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     steps += k;
                     status = ST_NEED;
                 } else if (a.prune) {
-                    U = __longlong_as_double(
-                        (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
+                    U = U_pre;
                 }
             }
             U = __shfl_sync(FULL, U, gshift);
