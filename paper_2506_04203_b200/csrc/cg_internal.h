@@ -62,7 +62,8 @@ struct RowTables {
     int nc;
     const int* probe_req; // [nc] request index of block i's smallest output
     double* Pv;           // [row][nc]
-    const unsigned* fut;  // [(na+1)][nc], na = arrival blocks of 32
+    const unsigned* fut;  // [(na+1)][nc], na = arrival blocks of fut_ab = 2^fut_sh requests
+    int fut_ab, fut_sh;
 };
 
 struct SimItem {

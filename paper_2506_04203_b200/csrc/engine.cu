@@ -191,6 +191,7 @@ struct cg_engine {
     std::vector<unsigned long long> ub_saved;
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
     int fut_block = 1;  // output-rank block of the future bound (option fut_block; 1 = exact counts)
+    int fut_arrival_shift = 5;  // log2 arrival block of the future bound (option fut_arrival: 1, 2, 4, ..., 32)
     int lane_check = 32;  // k_lane request-steps between prune checks (option lane_check: 8, 16, 32, 64)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
@@ -353,7 +354,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         // counts), arrivals in blocks of 32 (the prune checks' granularity)
         const int RB = E.fut_block;
         const int nc = (n_req + RB - 1) / RB;
-        const int na = (n_req + 31) / 32;
+        const int AB = 1 << E.fut_arrival_shift;  // arrival block (option fut_arrival: 1 = exact step)
+        const int na = (n_req + AB - 1) / AB;
         std::vector<int> probe(nc);
         for (int i = 0; i < nc; ++i) probe[i] = desc[std::min(RB * i + RB - 1, n_req - 1)];
         // fut[c][i] = #requests j >= 32c whose output rank block pos[j]/RB <= i,
@@ -364,7 +366,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             std::vector<unsigned> h(nc);
             for (int c = na - 1; c >= 0; --c) {
                 std::fill(h.begin(), h.end(), 0u);
-                for (int j = 32 * c; j < std::min(32 * c + 32, n_req); ++j) ++h[pos[j] / RB];
+                for (int j = AB * c; j < std::min(AB * c + AB, n_req); ++j) ++h[pos[j] / RB];
                 unsigned run = 0;
                 for (int i = 0; i < nc; ++i) {
                     run += h[i];
@@ -380,6 +382,8 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         x.h2d(dfut, fut.data(), fut.size() * sizeof(unsigned));
         tab.nc = E.fut_bound ? nc : 0;
         tab.probe_req = dprobe;
+        tab.fut_ab = AB;
+        tab.fut_sh = E.fut_arrival_shift;
         tab.fut = dfut;
         tab.Pv = E.d_pv.as<double>((size_t)nrows * nc);
     }
@@ -1971,6 +1975,12 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
         else if (k == "k4_pack") e->k4_pack = (int)value;
         else if (k == "fut_bound") e->fut_bound = (int)value;
         else if (k == "fut_block") e->fut_block = (int)std::min<int64_t>(1024, std::max<int64_t>(1, value));
+        else if (k == "fut_arrival") {
+            int sh = 0;
+            while ((1 << sh) < value && sh < 5) ++sh;
+            if (value < 1 || (1 << sh) != value) fail(CG_ERR_INVALID_INPUT, "fut_arrival must be 1, 2, 4, 8, 16 or 32");
+            e->fut_arrival_shift = sh;
+        }
         else if (k == "lane_check") {
             if (value != 8 && value != 16 && value != 32 && value != 64) fail(CG_ERR_INVALID_INPUT, "lane_check must be 8, 16, 32 or 64");
             e->lane_check = (int)value;

@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
             bool urefresh = false;
             if (status == ST_RUN) {
                 // requests still to come whose service alone exceeds U
-                const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + 31) >> 5) * a.tab.nc + (qi - 1)] : 0;
+                const int fut = qi > 0 ? (int)a.tab.fut[(long long)((k + a.tab.fut_ab - 1) >> a.tab.fut_sh) * a.tab.nc + (qi - 1)] : 0;
                 if (ov) {
                     if (gl == 0) {
                         const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
@@ -1105,7 +1105,8 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
         int fut_pre = 0;
         double U_pre = U;
         if (check_trip && status == ST_RUN) {
-            if (qi > 0) fut_pre = (int)a.tab.fut[(long long)((k + UNROLL + 31) >> 5) * a.tab.nc + (qi - 1)];
+            if (qi > 0)
+                fut_pre = (int)a.tab.fut[(long long)((k + UNROLL + a.tab.fut_ab - 1) >> a.tab.fut_sh) * a.tab.nc + (qi - 1)];
             if (a.prune)
                 U_pre = __longlong_as_double(
                     (long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus]);
