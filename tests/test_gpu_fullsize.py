@@ -64,3 +64,24 @@ def test_c3_cascade_reduced_trace_n40_vs_reference(engine):
     ref = _ref_sweep(t, cfg, N)
     d = diff_json(got, ref)
     assert not d, d[:8]
+
+
+C3_FIXTURE = os.path.join(os.path.dirname(__file__), "golden", "c3_full.json")
+
+
+@pytest.mark.skipif(not os.path.exists(C3_FIXTURE), reason="tools/make_c3_golden.py not run")
+def test_full_c3_sweep_vs_reference_fixture(engine):
+    """The bench workload itself: the full C3 sweep (1M requests, N = 64,
+    1.03e9 plans) against the unmodified reference's SweepResult, recorded by
+    tools/make_c3_golden.py (the reference needs about an hour for it)."""
+    import json
+    with open(C3_FIXTURE) as f:
+        fx = json.load(f)
+    t = W.build_trace("C3", eng.generate_trace)
+    cfg, N = W.planner_config("C3", t["scores"])
+    assert cfg == fx["config"] and N == fx["total_gpus"]
+    got = _ours(engine, t, cfg, N)
+    st = dict(engine.last_stats)
+    assert st["plans_enumerated"] == 1029930176 and st["unique_rows"] == 111
+    d = diff_json(got, fx["result"])
+    assert not d, d[:8]
