@@ -1123,13 +1123,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             // time is known
             unsigned mn = 0;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                // finish times and arrivals are non-negative doubles (or +inf): their
-                // bit patterns order like the values, so the idle scan runs on the
-                // integer pipe instead of the narrower fp64 one
-                const long long tb = __double_as_longlong(tn1);
-                mn |= (__double_as_longlong(av_get(r)) <= tb) ? (1u << r) : 0u;
-            }
+            for (int r = 0; r < R; ++r) mn |= (av_get(r) <= tn1) ? (1u << r) : 0u;
             // a sojourn counts toward the prune test only while the FIFOs are
             // intact (no ring overflow in the group so far)
             const bool intact = W == 1 ? !ovf : ((__ballot_sync(FULL, ovf) >> gshift) & wmask) == 0u;
