@@ -1038,6 +1038,15 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     const long long rb = (long long)row * kMaxShapes;
                     Trow = a.tab.T + (long long)row * a.tab.ld;
                     Orow = a.tab.O + (long long)row * a.tab.ld;
+                    // the new row's first arrivals/outputs and live bound depend on the
+                    // row alone: issue them before the replica set-up so their L2
+                    // latency overlaps it
+                    tq = *reinterpret_cast<const double2*>(Trow);
+                    oq = *reinterpret_cast<const double2*>(Orow);
+                    tq2 = *reinterpret_cast<const double2*>(Trow + (n_req > 2 ? 2 : 0));
+                    oq2 = *reinterpret_cast<const double2*>(Orow + (n_req > 2 ? 2 : 0));
+                    U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus])
+                                : INF;
                     // replicas j = gl*R + r in parts order: one merged pass
                     int q = 0, cum = 0, sh = -1;
                     const int np = gs.nparts;
@@ -1084,12 +1093,6 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     lbk = gs.lbk;
                     ovf = false;
                     lazy = 0;
-                    tq = *reinterpret_cast<const double2*>(Trow);
-                    oq = *reinterpret_cast<const double2*>(Orow);
-                    tq2 = *reinterpret_cast<const double2*>(Trow + (n_req > 2 ? 2 : 0));
-                    oq2 = *reinterpret_cast<const double2*>(Orow + (n_req > 2 ? 2 : 0));
-                    U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus])
-                                : INF;
                 }
             }
             __syncwarp();
