@@ -6,9 +6,14 @@
 // compares the output files byte for byte.
 //
 //   dropin_check <config.json> <trace-spec.json> <seed> <out_dir> [min_quality]
+//   dropin_check <config.json> <trace.jsonl> 0 <out_dir> <min_quality> --gpu-only [reps]
 //
 // Writes <out_dir>/{gpu,cpu}/{plan.json,front.json,front.csv,sweep.json} and
 // prints one JSON line {"identical": bool, "files": {...}, "gpu_s":..,"cpu_s":..}.
+// --gpu-only times the GPU-served pipeline alone (the CPU sweep of a large
+// config takes tens of minutes): cmd_plan end to end (JSONL ingest, sweep,
+// output files) and outerplan::sweep through the C++ binding on the parsed
+// records (AoS -> SoA, pageable copies, SweepResult rebuild), `reps` times.
 #include <chrono>
 #include <cstdio>
 #include <filesystem>
@@ -52,13 +57,48 @@ int main(int argc, char** argv) {
     const std::string cfg_path = argv[1], spec_path = argv[2], out = argv[4];
     const uint64_t seed = std::stoull(argv[3]);
     const double min_q = argc > 5 ? std::stod(argv[5]) : 0.0;
+    const bool gpu_only = argc > 6 && std::string(argv[6]) == "--gpu-only";
+    const int reps = argc > 7 ? std::stoi(argv[7]) : 3;
     namespace fs = std::filesystem;
     fs::create_directories(out + "/gpu");
     fs::create_directories(out + "/cpu");
-    auto spec = json::parse(slurp(spec_path)).get<cli::TraceGenSpec>();
-    auto trace = cli::generate_trace(spec, seed);
-    const std::string trace_path = out + "/trace.jsonl";
-    write_trace_jsonl(trace_path, trace);
+    std::string trace_path = out + "/trace.jsonl";
+    if (spec_path.size() > 6 && spec_path.substr(spec_path.size() - 6) == ".jsonl") {
+        trace_path = spec_path;  // a prepared trace (e.g. C3's concatenated bursty segments)
+    } else {
+        auto spec = json::parse(slurp(spec_path)).get<cli::TraceGenSpec>();
+        auto trace = cli::generate_trace(spec, seed);
+        write_trace_jsonl(trace_path, trace);
+    }
+    if (gpu_only) {
+        cli::PlanArgs args;
+        args.config_path = cfg_path;
+        args.trace_path = trace_path;
+        args.out_dir = out + "/gpu";
+        args.min_quality = min_q;
+        json report;
+        std::vector<double> plan_s, sweep_s;
+        auto cfg = cli::load_planner_config(cfg_path);
+        auto tr = read_trace_jsonl(trace_path);  // GPU ingest (warm-up of the engine too)
+        for (int i = 0; i < reps + 1; ++i) {
+            auto t0 = std::chrono::steady_clock::now();
+            cli::cmd_plan(args);
+            const double a = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            t0 = std::chrono::steady_clock::now();
+            auto res = outerplan::sweep(tr, cfg.models, cfg.hardware, cfg.cost_model, cfg.hardware.gpu_count, cfg.sweep);
+            const double b = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (i > 0) {  // the first pass warms up the engine's buffers
+                plan_s.push_back(a);
+                sweep_s.push_back(b);
+            }
+            if (res.evaluations.empty() && res.skipped.empty()) std::fprintf(stderr, "empty sweep\n");
+        }
+        report["records"] = tr.size();
+        report["cmd_plan_s"] = plan_s;
+        report["sweep_binding_s"] = sweep_s;
+        std::cout << report.dump() << std::endl;
+        return 0;
+    }
 
     // GPU: the reference CLI pipeline, whose sweep() call now lands in the engine.
     cli::PlanArgs args;
