@@ -194,6 +194,7 @@ struct cg_engine {
     int fut_arrival_shift = 5;  // log2 arrival block of the future bound (option fut_arrival: 1, 2, 4, ..., 32)
     int lane_check = 32;  // k_lane request-steps between prune checks (option lane_check: 8, 16, 32, 64)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
+    int seeds = 1;      // homogeneous seed plans of the heavy rows first (option seeds)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
     int pilot_merge = 1;            // pilot launches: see PilotArgs::merge (option pilot_merge)
     int pilot_sort = 1;             // pilot lists in ascending estimate order (option pilot_sort)
@@ -620,7 +621,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         ++x.launches;
         ++x.st.collectives;
     };
-    if (E.prune) {
+    if (E.prune && E.seeds) {
         int seed_no = 0;
         for (int r = 0; r < nrows; ++r) {
             const auto& sp = hs[rows[r].space];
@@ -1986,6 +1987,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
             e->lane_check = (int)value;
         }
         else if (k == "pilot") e->pilot = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));
+        else if (k == "seeds") e->seeds = value ? 1 : 0;
         else if (k == "sort_key") e->sort_key = (int)value;
         else if (k == "class_order") e->class_order = (int)value;
         else if (k == "pilot_min_plans") e->pilot_min_plans = std::max<int64_t>(0, value);
