@@ -829,6 +829,47 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
     const long long rb = (long long)row * kMaxShapes;
     int np = (int)(w0 & 15ull);
     int dp = 0, used = 0;
+    if (rec && np > 0 && !a.check_stable) {
+        // filtered item with its parts: decode them into registers (unrolled, so
+        // the part offsets are constants) and issue the live bound and every
+        // part's bound-snapshot entry at once -- independent loads, one latency
+        unsigned shp[kRecMaxParts];
+#pragma unroll
+        for (int q = 0; q < kRecMaxParts; ++q) {
+            shp[q] = 0u;
+            if (q < np) {
+                const unsigned v = rec_part(w0, w1, w2, q);
+                shp[q] = v & 31u;
+                gs.pshape[q] = (unsigned char)(v & 31u);
+                gs.pcount[q] = (unsigned char)(v >> 5);
+                dp += (int)(v >> 5);
+            }
+        }
+        used = (int)((w0 >> 4) & 511ull);
+        const long long cell = (long long)row * (a.N + 1) + used;
+        const double U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[cell])
+                                 : __longlong_as_double(0x7ff0000000000000ll);
+        const bool useq = a.prune && a.qtab && a.tab.nc > 0;
+        const unsigned short* qt = useq ? a.qtab + cell * kMaxShapes : nullptr;
+        int qv[kRecMaxParts];
+#pragma unroll
+        for (int q = 0; q < kRecMaxParts; ++q) qv[q] = (useq && q < np) ? (int)qt[shp[q]] : (1 << 30);
+        if (a.prune && lb > U) {
+            ++bound;
+            return false;
+        }
+        int qi = 1 << 30;
+#pragma unroll
+        for (int q = 0; q < kRecMaxParts; ++q) qi = qv[q] < qi ? qv[q] : qi;
+        gs.nparts = np;
+        gs.row = row;
+        gs.plan = plan;
+        gs.dp = dp;
+        gs.used = used;
+        gs.qi = (useq && qi != (1 << 30)) ? qi : 0;
+        gs.lbk = lb;
+        return true;
+    }
     if (np > 0) {
         for (int q = 0; q < np; ++q) {
             const unsigned v = rec_part(w0, w1, w2, q);
@@ -1047,9 +1088,31 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     oq2 = *reinterpret_cast<const double2*>(Orow + (n_req > 2 ? 2 : 0));
                     U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[(long long)row * (a.N + 1) + gpus])
                                 : INF;
-                    // replicas j = gl*R + r in parts order: one merged pass
+                    // replicas j = gl*R + r in parts order.  With the parts listed
+                    // (np > 0) replica j's part is the number of part starts <= j:
+                    // independent shared-memory reads instead of a serial walk
                     int q = 0, cum = 0, sh = -1;
                     const int np = gs.nparts;
+                    unsigned ps = 0u;  // bit j: replica j starts a part
+                    if (np > 0) {
+                        int c0 = 0;
+#pragma unroll
+                        for (int qq = 0; qq < kGsParts; ++qq)
+                            if (qq < np) {
+                                if (c0 < 32) ps |= 1u << c0;
+                                c0 += gs.pcount[qq];
+                            }
+                        if (SA) {
+#pragma unroll
+                            for (int qq = 0; qq < kGsParts; ++qq)
+                                if (qq < np) {
+                                    const int shq = gs.pshape[qq];
+                                    pre_s[qq * 32 + lane] = a.tab.prefill[rb + shq];
+                                    dec_s[qq * 32 + lane] = a.tab.decode[rb + shq];
+                                }
+                            pstart = ps;
+                        }
+                    }
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
@@ -1059,16 +1122,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                         prev_s[r * 32 + lane] = INF;
                         if (j < dp) {
                             if (np > 0) {
-                                while (j >= cum) {
-                                    sh = gs.pshape[q];
-                                    cum += gs.pcount[q];
-                                    if (SA) {
-                                        pre_s[q * 32 + lane] = a.tab.prefill[rb + sh];
-                                        dec_s[q * 32 + lane] = a.tab.decode[rb + sh];
-                                        pstart |= 1u << r;
-                                    }
-                                    ++q;
-                                }
+                                sh = gs.pshape[__popc(ps & ((2u << j) - 1u)) - 1];
                             } else {
                                 while (j >= cum) {
                                     ++sh;
