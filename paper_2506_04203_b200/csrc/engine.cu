@@ -534,23 +534,46 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         unsigned long long novf[8];
         x.d2h(novf, ovfcnt, sizeof(novf));
         x.sync();
+        // one launch per class; the classes' launches are independent (own
+        // item counter, scratch region and rings), so they run concurrently on
+        // the engine's streams -- each is a few hundred plans with full request
+        // chains, latency-bound on its own
+        size_t ring_each = 0;
         for (int cls = 0; cls < 7; ++cls) {
             if (novf[cls] == 0) continue;
             if (novf[cls] > ovf_region) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
             x.st.plans_overflow += (long long)novf[cls];
             SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
-            double* ring = E.d_ring.as<double>((size_t)gd.warps * 32 * gd.R * ring_cap);
-            CG_CUDA(cudaMemsetAsync(ictr, 0, 8, x.s));
-            CG_CUDA(cudaMemsetAsync(ovfcnt2, 0, 8, x.s));
+            ring_each = std::max(ring_each, (size_t)gd.warps * 32 * gd.R * ring_cap);
+        }
+        if (ring_each == 0) return;
+        double* ring = E.d_ring.as<double>(ring_each * nregions);
+        unsigned long long* oc2 = E.d_ovfcnt2.as<unsigned long long>((size_t)nregions);
+        cudaStream_t streams[4] = {x.s, E.s2, E.s3, E.s4};
+        CG_CUDA(cudaEventRecord(E.ev[12], x.s));
+        int launched = 0;
+        for (int cls = 0; cls < 7; ++cls) {
+            if (novf[cls] == 0) continue;
+            const int k = launched++ % nregions;
+            cudaStream_t st = streams[k];
+            if (k > 0 && launched <= nregions) CG_CUDA(cudaStreamWaitEvent(st, E.ev[12], 0));
+            CG_CUDA(cudaMemsetAsync(ictr + k, 0, 8, st));
+            CG_CUDA(cudaMemsetAsync(oc2 + k, 0, 8, st));
             SimArgs d = base;
             d.items = ovf + (size_t)cls * ovf_region;
             d.recs = nullptr;
             d.perm = nullptr;
             d.nitems = novf[cls];
-            d.ring_global = ring;
+            d.item_counter = ictr + k;
+            d.scratch = scratch + (size_t)k * max_slots * sld;
+            d.ring_global = ring + (size_t)k * ring_each;
             d.ovf = ovf + (size_t)7 * ovf_region;  // cannot overflow (capacity >= n_req)
-            d.ovf_count = ovfcnt2;
-            launch_sim(d, cls, SIM_DEEP, E.sm_count, x.s, &x.launches, nullptr);
+            d.ovf_count = oc2 + k;
+            launch_sim(d, cls, SIM_DEEP, E.sm_count, st, &x.launches, nullptr);
+        }
+        for (int k = 1; k < nregions && k < launched; ++k) {
+            CG_CUDA(cudaEventRecord(E.ev[12 + k], streams[k]));
+            CG_CUDA(cudaStreamWaitEvent(x.s, E.ev[12 + k], 0));
         }
     };
 
@@ -597,8 +620,12 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         return (double)coff[7] * (sizeof(ItemRec) + 8) + (double)cmax * (sizeof(ItemRec) + 40);
     };
     {
+        // the list buffers this engine already holds are reused, so they count
+        // as available: the wave size does not depend on earlier sweeps
         size_t fr = 0, tot = 0;
-        const double budget = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? 0.6 * (double)fr : 64e9;
+        const double held = (double)(E.d_lrecs.bytes + E.d_lkeys.bytes + E.d_lidx.bytes + E.d_lk1.bytes +
+                                     E.d_lv1.bytes + E.d_grecs.bytes);
+        const double budget = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? 0.6 * ((double)fr + held) : 64e9;
         while (size_lists() > budget && wave_chunks > 1) wave_chunks = (wave_chunks + 1) / 2;
     }
     const unsigned long long nwaves = (max_chunks + wave_chunks - 1) / wave_chunks;
