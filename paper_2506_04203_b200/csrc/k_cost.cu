@@ -73,8 +73,10 @@ __global__ void k_row_shapes(RowSetupArgs a) {
     const RowDesc rd = a.rows[row];
     const PlanSpace& sp = a.spaces[rd.space];
     const long long o = (long long)row * kMaxShapes + s;
-    if (s >= sp.S) {
+    if (s >= sp.S) {  // no such shape: defined values all the same (tables are read per row, 32 wide)
         a.tab.shape_ok[o] = 0;
+        a.tab.prefill[o] = a.tab.decode[o] = a.tab.mean_service[o] = 0.0;
+        a.tab.inv_service[o] = __longlong_as_double(0x7ff8000000000000ll);
         return;
     }
     const ModelArgs m = a.models[rd.stage];
