@@ -538,13 +538,19 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
         // item counter, scratch region and rings), so they run concurrently on
         // the engine's streams -- each is a few hundred plans with full request
         // chains, latency-bound on its own
+        // each launch is sized to its overflow count (one plan per group of
+        // W lanes): the global rings are 16 KB per lane-replica slot
         size_t ring_each = 0;
+        int sms[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int cls = 0; cls < 7; ++cls) {
             if (novf[cls] == 0) continue;
             if (novf[cls] > ovf_region) fail(CG_ERR_CUDA, "JSQ overflow list exhausted");
             x.st.plans_overflow += (long long)novf[cls];
             SimGeometry gd = sim_geometry(cls, SIM_DEEP, E.sm_count);
-            ring_each = std::max(ring_each, (size_t)gd.warps * 32 * gd.R * ring_cap);
+            const long long per_sm_groups = std::max<long long>(1, gd.warps * gd.G / E.sm_count);
+            sms[cls] = (int)std::min<long long>(E.sm_count, ((long long)novf[cls] + per_sm_groups - 1) / per_sm_groups);
+            const long long warps = gd.warps / E.sm_count * sms[cls];
+            ring_each = std::max(ring_each, (size_t)warps * 32 * gd.R * ring_cap);
         }
         if (ring_each == 0) return;
         double* ring = E.d_ring.as<double>(ring_each * nregions);
@@ -569,7 +575,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
             d.ring_global = ring + (size_t)k * ring_each;
             d.ovf = ovf + (size_t)7 * ovf_region;  // cannot overflow (capacity >= n_req)
             d.ovf_count = oc2 + k;
-            launch_sim(d, cls, SIM_DEEP, E.sm_count, st, &x.launches, nullptr);
+            launch_sim(d, cls, SIM_DEEP, sms[cls], st, &x.launches, nullptr);
         }
         for (int k = 1; k < nregions && k < launched; ++k) {
             CG_CUDA(cudaEventRecord(E.ev[12 + k], streams[k]));
