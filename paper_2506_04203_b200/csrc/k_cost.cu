@@ -39,6 +39,7 @@
 #include "cg_internal.h"
 #include "cg_kernels.h"
 #include "plan_dev.cuh"
+#include "cg_ptx.cuh"
 
 namespace cg {
 
@@ -131,11 +132,20 @@ __global__ void k_row_crn(RowSetupArgs a, const double* __restrict__ L) {
 
 enum : int { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2, ST_FINISH = 3 };
 
+#ifndef CG_PF
+#define CG_PF 1
+#endif
+#ifndef CG_SELBIT
+#define CG_SELBIT 1
+#endif
+#ifndef CG_AS_MIN
+#define CG_AS_MIN 32
+#endif
 constexpr int kGsParts = 16;  // parts held in GroupShared (>= kRecMaxParts)
 
 struct GroupShared {
     unsigned long long plan;  // current plan index
-    unsigned long long hi;    // end of current item (exclusive)
+    unsigned long long hi;    // k_lane: the pre-claimed next record's item (cp.async target)
     double lbk;   // the plan's service bound: sojourns below it never reach the p95
     int row;
     int used;   // GPUs of the current count vector
@@ -146,7 +156,10 @@ struct GroupShared {
     int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
     int qi;       // future-bound blocks of the plan (SimArgs::qtab)
     unsigned char pshape[kGsParts], pcount[kGsParts];
-    unsigned char counts[kMaxShapes];
+    union {
+        unsigned char counts[kMaxShapes];  // k_sim: count vector of the current plan
+        unsigned long long pfw[4];         // k_lane: the next record's parts words and service bound
+    };
 };
 
 // ItemRec part stream (cg_kernels.h): header (np, used) then 13-bit parts.
@@ -778,6 +791,22 @@ __global__ void __launch_bounds__(128, R <= 2 ? 6 : 3) k_sim(SimArgs a) {
 //   * plans are claimed with one warp-aggregated atomic per round; the K-th
 //     largest selection is warp-cooperative, one finished plan at a time.
 // Exactness is that of k_sim: same operations in the same order per request.
+#ifdef CG_K4_PROF
+// development counters (CG_BUILD_VARIANT=prof): per R class (4/8/16/32) of the
+// one-lane-per-plan kernels: cycles per phase and event counts, summed over warps
+__device__ unsigned long long g_k4prof[4][16];
+#define K4P_DECL unsigned long long p_[16] = {}; long long pt_ = clock64(), pt0_ = pt_;
+#define K4P_MARK(i) do { const long long c_ = clock64(); p_[i] += (unsigned long long)(c_ - pt_); pt_ = c_; } while (0)
+#define K4P_ADD(i, v) (p_[i] += (unsigned long long)(v))
+#define K4P_FLUSH(ri) do { p_[0] = (unsigned long long)(clock64() - pt0_); p_[11] = 1; if (lane == 0) \
+    for (int i_ = 0; i_ < 16; ++i_) atomicAdd(&g_k4prof[ri][i_], p_[i_]); } while (0)
+#else
+#define K4P_DECL
+#define K4P_MARK(i) do {} while (0)
+#define K4P_ADD(i, v) do {} while (0)
+#define K4P_FLUSH(ri) do {} while (0)
+#endif
+
 template <int W, int R>
 struct LaneTraits {
     static constexpr int G = 32 / W;
@@ -795,14 +824,17 @@ struct LaneTraits {
     // and prefill/decode per part of the plan (<= kGsParts) so the footprint
     // still fits two 2-warp blocks per SM
     static constexpr bool SA = W == 1 && R >= 32;
+    // AS: replica finish times in shared memory (SA, and R >= CG_AS_MIN)
+    static constexpr bool AS = W == 1 && R >= CG_AS_MIN;
     static constexpr int PD = SA ? kGsParts : R;  // prefill/decode slots per lane
     static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
     // prefill, decode, head-job finish, previous-job finish (per replica slot)
-    static constexpr size_t pd_bytes = (size_t)(2 * PD + (SA ? 3 : 2) * R) * 32 * sizeof(double);
+    static constexpr size_t pd_bytes = (size_t)(2 * PD + (AS ? 3 : 2) * R) * 32 * sizeof(double);
     static constexpr size_t ht_bytes = (size_t)R * 32 * sizeof(unsigned);  // ring head | tail << 16
     static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
     static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + ht_bytes + hist_bytes + G * sizeof(GroupShared);
+    static_assert(hist_bytes >= (size_t)G * kMaxShapes, "count-vector scratch in the histogram area");
 };
 
 // Claims work item `it` into gs; false when the item is rejected (an unstable
@@ -810,20 +842,11 @@ struct LaneTraits {
 // carry their parts and service bound, so a claim is one round of
 // independent loads (the record) and one dependent one (the live bound and
 // the plan's future-bound blocks, SimArgs::qtab).
-__device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long slot, unsigned long long& bound) {
-    unsigned long long item, w0 = 0ull, w1 = 0ull, w2 = 0ull;
-    double lb = 0.0;
-    const bool rec = a.recs != nullptr;
-    if (rec) {
-        const ItemRec& r = a.recs[slot];
-        item = r.item;
-        w0 = r.w[0];
-        w1 = r.w[1];
-        w2 = r.w[2];
-        lb = r.lb;
-    } else {
-        item = a.items[slot];
-    }
+// `counts`: the lane's count-vector scratch (unranked plans with more parts
+// than a record lists).
+__device__ bool lane_take_r(const SimArgs& a, GroupShared& gs, unsigned char* counts, unsigned long long item,
+                            unsigned long long w0, unsigned long long w1, unsigned long long w2, double lb,
+                            const bool rec, unsigned long long& bound) {
     const int row = (int)(item >> kItemPlanBits);
     const unsigned long long plan = item & kItemPlanMask;
     const RowDesc& rd = a.rows[row];
@@ -881,9 +904,9 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
         }
         used = (int)((w0 >> 4) & 511ull);
     } else {
-        used = unrank_plan(sp, plan, gs.counts);
+        used = unrank_plan(sp, plan, counts);
         for (int s = 0; s < sp.S; ++s) {
-            const int c = gs.counts[s];
+            const int c = counts[s];
             if (!c) continue;
             if (np < kGsParts) {
                 gs.pshape[np] = (unsigned char)s;
@@ -898,7 +921,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
         double capacity = 0.0;
         for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
             const int sh = np > 0 ? gs.pshape[q] : s;
-            const int c = np > 0 ? gs.pcount[q] : gs.counts[s];
+            const int c = np > 0 ? gs.pcount[q] : counts[s];
             if (!c) continue;
             if (!a.tab.shape_ok[rb + sh]) return false;
             capacity = __dadd_rn(capacity, __ddiv_rn((double)c, a.tab.mean_service[rb + sh]));
@@ -911,7 +934,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
         double m = __longlong_as_double(0x7ff0000000000000ll);
         for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
             const int sh = np > 0 ? gs.pshape[q] : s;
-            if (np == 0 && !gs.counts[s]) continue;
+            if (np == 0 && !counts[s]) continue;
             const double v = a.tab.prefill[rb + sh] + o_k * a.tab.decode[rb + sh];
             m = v < m ? v : m;
         }
@@ -931,7 +954,7 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
         qi = 1 << 30;
         for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
             const int sh = np > 0 ? gs.pshape[q] : s;
-            if (np == 0 && !gs.counts[s]) continue;
+            if (np == 0 && !counts[s]) continue;
             const int v = qt[sh];
             qi = v < qi ? v : qi;
         }
@@ -946,6 +969,31 @@ __device__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned long long 
     gs.lbk = lb;
     return true;
 }
+
+// (mask & bit) ? a : b as a predicate from one bit test and a selp: opaque to
+// the front end, so it is not re-derived into compare-and-select chains
+__device__ __forceinline__ double sel_bit(unsigned mask, unsigned bit, double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t"
+        "selp.f64 %0, %3, %4, p;\n\t}"
+        : "=d"(r)
+        : "r"(mask), "r"(bit), "d"(a), "d"(b));
+    return r;
+}
+
+__device__ __forceinline__ bool lane_take(const SimArgs& a, GroupShared& gs, unsigned char* counts,
+                                          unsigned long long slot, unsigned long long& bound) {
+    if (a.recs) {
+        const ItemRec& r = a.recs[slot];
+        return lane_take_r(a, gs, counts, r.item, r.w[0], r.w[1], r.w[2], r.lb, true, bound);
+    }
+    return lane_take_r(a, gs, counts, a.items[slot], 0ull, 0ull, 0ull, 0.0, false, bound);
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // request-steps between exact-bound prune checks: SimArgs::lane_check (engine option lane_check)
 
@@ -968,6 +1016,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     double* pre_s = reinterpret_cast<double*>(wbase + TR::ring_bytes);
     constexpr int PD = TR::PD;
     constexpr bool SA = TR::SA;
+    constexpr bool AS = TR::AS;
     double* dec_s = pre_s + PD * 32;
     double* nd_s = dec_s + PD * 32;  // finish time of each replica's head job (INF: none)
     // finish of the job before each replica's last one (INF: no replica; a
@@ -982,6 +1031,13 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes +
                                                       TR::hist_bytes);
     GroupShared& gs = gsa[gid];
+    // the group's count-vector scratch lives in the warp's histogram area (used
+    // only by the phase-D selection; phase A is done with it by then), so the
+    // GroupShared count bytes can hold the prefetched next record
+    unsigned char* const lcounts = reinterpret_cast<unsigned char*>(hist) + gid * kMaxShapes;
+    // record prefetch (W = 1 lists of filtered records in list order)
+    const bool pfm = CG_PF && W == 1 && a.recs != nullptr && a.perm == nullptr && !a.check_stable;
+    int pf_st = 0;  // 0: no next record claimed yet, 1: next record copied into gs, 2: list exhausted
 
     const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
     double* const scratch = a.scratch + (gwarp * G + gid) * (long long)a.sld;
@@ -1007,14 +1063,14 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     // per replica: avail = finish of its last job (registers: every step's
     // idle mask reads them all); the head job's finish (nd_s), the previous
     // job's finish (prev_s) and the ring head/tail (ht_s) live in shared memory
-    double avail[SA ? 1 : R];
+    double avail[AS ? 1 : R];
     // finish of replica r's last job
     auto av_get = [&](int r) -> double {
-        if constexpr (SA) return avail_s[r * 32 + lane];
+        if constexpr (AS) return avail_s[r * 32 + lane];
         else return avail[r];
     };
     auto av_set = [&](int r, double v) {
-        if constexpr (SA) avail_s[r * 32 + lane] = v;
+        if constexpr (AS) avail_s[r * 32 + lane] = v;
         else avail[r] = v;
     };
     unsigned pstart = 0;  // SA: bit r set when replica r starts a new part
@@ -1039,30 +1095,95 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
         prev_s[r * 32 + lane] = INF;
     }
     unsigned long long steps = 0, full = 0, pruned = 0, bound = 0;
+    K4P_DECL
 
     for (unsigned it = 0;; ++it) {
         // ---- phase A: groups without a plan claim one (one atomic per round)
         const bool need = status == ST_NEED;
+        K4P_MARK(2);
         if (__any_sync(FULL, need)) {
+            K4P_ADD(5, 1);
             bool want = need && gl == 0;
             unsigned m = __ballot_sync(FULL, want);
             while (m) {
-                const int ldr = __ffs(m) - 1;
-                unsigned long long base = 0;
-                if (lane == ldr) base = atomicAdd(a.item_counter, (unsigned long long)__popc(m));
-                base = __shfl_sync(FULL, base, ldr);
+                K4P_ADD(6, 1);
+                K4P_ADD(8, __popc(m));
                 bool again = false;
-                if (want) {
-                    const unsigned long long item = base + __popc(m & ((1u << lane) - 1u));
-                    if (item >= a.nitems) gs.status = ST_DONE;
-                    else if (lane_take(a, gs, a.perm ? (unsigned long long)a.perm[item] : item, bound))
-                        gs.status = ST_RUN;
-                    else again = true;
+                if (pfm) {
+                    // record prefetch: a lane takes its pre-claimed record (copied
+                    // into shared memory during its previous plan) and claims the
+                    // next one; a lane without one (its first claim) claims two.
+                    // The atomic's result is needed only to issue the next copy,
+                    // after the take, so neither the atomic nor the record load is
+                    // on the claim's critical path.
+                    const unsigned c1 = __ballot_sync(FULL, want && pf_st == 1);
+                    const unsigned c2 = __ballot_sync(FULL, want && pf_st == 0);
+                    const unsigned call = c1 | c2;
+                    const int ldr = call ? __ffs(call) - 1 : 0;
+                    unsigned long long base = 0;
+                    if (call && lane == ldr)
+                        base = atomicAdd(a.item_counter, (unsigned long long)(__popc(c1) + 2 * __popc(c2)));
+                    const unsigned lt = (1u << lane) - 1u;
+                    const unsigned long long off = (unsigned long long)(__popc(c1 & lt) + 2 * __popc(c2 & lt));
+                    if (c2) base = __shfl_sync(FULL, base, ldr);  // first claims only
+                    if (want) {
+                        bool have = false;
+                        unsigned long long it0 = 0ull, w0 = 0ull, w1 = 0ull, w2 = 0ull;
+                        double lb = 0.0;
+                        if (pf_st == 1) {
+                            cp_async_wait_all();
+                            it0 = gs.hi;
+                            w0 = gs.pfw[0];
+                            w1 = gs.pfw[1];
+                            w2 = gs.pfw[2];
+                            lb = __longlong_as_double((long long)gs.pfw[3]);
+                            have = true;
+                        } else if (pf_st == 0 && base + off < a.nitems) {
+                            const ItemRec& r = a.recs[base + off];
+                            it0 = r.item;
+                            w0 = r.w[0];
+                            w1 = r.w[1];
+                            w2 = r.w[2];
+                            lb = r.lb;
+                            have = true;
+                        }
+                        if (!have) gs.status = ST_DONE;
+                        else if (lane_take_r(a, gs, lcounts, it0, w0, w1, w2, lb, true, bound)) gs.status = ST_RUN;
+                        else again = true;
+                    }
+                    if (c1) base = __shfl_sync(FULL, base, ldr);
+                    if ((call >> lane) & 1u) {
+                        const unsigned long long nx = base + off + ((c2 >> lane) & 1u);
+                        if (nx < a.nitems) {
+                            const ItemRec* r = a.recs + nx;
+                            cp_async8(&gs.hi, &r->item);
+                            cp_async8(&gs.pfw[0], &r->w[0]);
+                            cp_async8(&gs.pfw[1], &r->w[1]);
+                            cp_async8(&gs.pfw[2], &r->w[2]);
+                            cp_async8(&gs.pfw[3], &r->lb);
+                            pf_st = 1;
+                        } else {
+                            pf_st = 2;
+                        }
+                    }
+                } else {
+                    const int ldr = __ffs(m) - 1;
+                    unsigned long long base = 0;
+                    if (lane == ldr) base = atomicAdd(a.item_counter, (unsigned long long)__popc(m));
+                    base = __shfl_sync(FULL, base, ldr);
+                    if (want) {
+                        const unsigned long long item = base + __popc(m & ((1u << lane) - 1u));
+                        if (item >= a.nitems) gs.status = ST_DONE;
+                        else if (lane_take(a, gs, lcounts, a.perm ? (unsigned long long)a.perm[item] : item, bound))
+                            gs.status = ST_RUN;
+                        else again = true;
+                    }
                 }
                 want = again;
                 m = __ballot_sync(FULL, want);
             }
             __syncwarp();
+            K4P_MARK(1);
             if (need) {
                 status = gs.status;
                 if (SA && status == ST_RUN && gs.nparts == 0) {
@@ -1128,7 +1249,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                             } else {
                                 while (j >= cum) {
                                     ++sh;
-                                    cum += gs.counts[sh];
+                                    cum += lcounts[sh];
                                 }
                             }
                             if (!SA) {
@@ -1152,9 +1273,13 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 }
             }
             __syncwarp();
+            K4P_ADD(7, __popc(__ballot_sync(FULL, need && status == ST_RUN)));
+            K4P_MARK(12);
         }
         if (__all_sync(FULL, status == ST_DONE)) break;
         U = __shfl_sync(FULL, U, gshift);  // one bound per group (leader's)
+        K4P_ADD(9, 1);
+        K4P_ADD(10, __popc(__ballot_sync(FULL, status == ST_RUN)));
 
         // a trip that ends with a prune check issues the check's loads now (the
         // future-bound count at the trip's end step and the live bound), so their
@@ -1295,7 +1420,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 if (busy) {
                     // avail of replica rr: select tree on rr's bits; its ring state from shared memory
                     H = ht_s[rr * 32 + lane];
-                    if constexpr (SA) {
+                    if constexpr (AS) {
                         start = avail_s[rr * 32 + lane];  // > t: std::max(t, avail)
                     } else {
                         double av[R];
@@ -1337,15 +1462,20 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     prev_s[rr * 32 + lane] = start;
                     ht_s[rr * 32 + lane] = H;
                 }
-                if constexpr (SA) {
+                if constexpr (AS) {
                     if (me) avail_s[rr * 32 + lane] = fin;
                 } else {
+                    // one-hot winner mask: a bit test and one 64-bit select per
+                    // replica (written as (me && r == rr) the compiler built the
+                    // new value and then selected it again: five instructions)
+                    const unsigned oh = me ? (1u << rr) : 0u;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) avail[r] = (me && r == rr) ? fin : avail[r];
+                    for (int r = 0; r < R; ++r)
+                        avail[r] = CG_SELBIT ? sel_bit(oh, 1u << r, fin, avail[r]) : ((me && r == rr) ? fin : avail[r]);
                 }
                 if (HO && first) {  // the job is the head of an empty ring (rarer than a step)
 #pragma unroll
-                    for (int r = 0; r < R; ++r) ho[r] = r == rr ? o : ho[r];
+                    for (int r = 0; r < R; ++r) ho[r] = sel_bit(1u << rr, 1u << r, o, ho[r]);
                 }
                 ab += (me && intact && soj > U) ? 1 : 0;
                 // only sojourns >= the service bound can be among the K largest
@@ -1394,6 +1524,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             }
         }
 
+        K4P_MARK(2);
         // ---- phase C: periodic exact-bound pruning and overflow checks
         if (check_trip) {
             int tot = ab;
@@ -1430,6 +1561,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             if (status == ST_NEED && gl == 0) gs.status = ST_NEED;
         }
 
+        K4P_MARK(3);
         // ---- phase D: completed plans -> exact p95 (warp-cooperative) and row bookkeeping
         if (__any_sync(FULL, status == ST_FINISH)) {
             int tot = ab;
@@ -1484,7 +1616,9 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             }
             __syncwarp();
         }
+        K4P_MARK(4);
     }
+    if constexpr (W == 1) K4P_FLUSH(R == 4 ? 0 : R == 8 ? 1 : R == 16 ? 2 : 3);
     if (gl == 0) {
         count_add(&a.counters[CTR_BOUND], bound);
         count_add(&a.counters[CTR_STEPS], steps);
@@ -2003,4 +2137,13 @@ void launch_resolve(const ResolveArgs& a, cudaStream_t s, int* launches) {
     }
 }
 
+#ifdef CG_K4_PROF
+extern "C" int cg_k4prof_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, cg::g_k4prof, sizeof(cg::g_k4prof)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int cg_k4prof_reset() {
+    static unsigned long long z[4][16] = {};
+    return cudaMemcpyToSymbol(cg::g_k4prof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif
 }  // namespace cg
