@@ -1054,6 +1054,8 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     unsigned long long plan = 0;
     bool ovf = false;
     unsigned lazy = 0;
+    unsigned valid = 0;  // replicas of the current plan on this lane
+    unsigned fresh = 0;  // AS: replicas not dispatched since the claim (their slots are stale)
     unsigned mcur = 0;  // this step's idle mask (avail[r] <= t), computed one step ahead
     double U = INF;
     const double* Trow = a.tab.T;  // valid dummies until a plan is acquired
@@ -1236,13 +1238,17 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                             pstart = ps;
                         }
                     }
+                    // no per-replica reset of the shared-memory state (head-job
+                    // finish, ring head/tail, previous finish, and with AS the
+                    // finish times): a replica's slots are written when it is first
+                    // dispatched, every read of them is masked by `valid`, and with
+                    // AS the idle scan treats `fresh` (never dispatched) replicas as
+                    // idle.  Until a replica is dispatched it is idle, so the busy
+                    // and FIFO paths only ever see dispatched replicas.
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
-                        nd_s[r * 32 + lane] = INF;
-                        ht_s[r * 32 + lane] = 0u;
-                        av_set(r, INF);
-                        prev_s[r * 32 + lane] = INF;
+                        if constexpr (!AS) av_set(r, INF);
                         if (j < dp) {
                             if (np > 0) {
                                 sh = gs.pshape[__popc(ps & ((2u << j) - 1u)) - 1];
@@ -1256,13 +1262,14 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                                 pre_s[r * 32 + lane] = a.tab.prefill[rb + sh];
                                 dec_s[r * 32 + lane] = a.tab.decode[rb + sh];
                             }
-                            av_set(r, 0.0);
-                            prev_s[r * 32 + lane] = 0.0;
+                            if constexpr (!AS) av_set(r, 0.0);
                         }
                     }
                     mcur = 0;  // every replica starts idle (avail 0 <= T[0])
 #pragma unroll
                     for (int r = 0; r < R; ++r) mcur |= (gl * R + r < dp) ? (1u << r) : 0u;
+                    valid = mcur;
+                    fresh = AS ? mcur : 0u;
                     k = 0;
                     ab = 0;
                     ns = 0;
@@ -1308,6 +1315,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             unsigned mn = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) mn |= (av_get(r) <= tn1) ? (1u << r) : 0u;
+            if constexpr (AS) mn = (mn & valid & ~fresh) | fresh;
             // a sojourn counts toward the prune test only while the FIFOs are
             // intact (no ring overflow in the group so far)
             const bool intact = W == 1 ? !ovf : ((__ballot_sync(FULL, ovf) >> gshift) & wmask) == 0u;
@@ -1338,7 +1346,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 unsigned m1 = 0;
 #pragma unroll
                 for (int r = 0; r < R; ++r) m1 |= (busy && prev_s[r * 32 + lane] <= t) ? (1u << r) : 0u;
-                m1 = busy ? m1 : 0u;
+                m1 = busy ? (m1 & valid) : 0u;
                 bool has1;
                 if (W == 1) {
                     has1 = m1 != 0u;
@@ -1370,6 +1378,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     unsigned dep = 0;
 #pragma unroll
                     for (int r = 0; r < R; ++r) dep |= (slow && nd_s[r * 32 + lane] <= t) ? (1u << r) : 0u;
+                    dep &= valid;
                     while (W == 1 ? dep != 0u : __any_sync(FULL, dep != 0u)) {
 #pragma unroll
                         for (int r = 0; r < R; ++r) {
@@ -1464,6 +1473,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 }
                 if constexpr (AS) {
                     if (me) avail_s[rr * 32 + lane] = fin;
+                    fresh &= me ? ~(1u << rr) : ~0u;
                 } else {
                     // one-hot winner mask: a bit test and one 64-bit select per
                     // replica (written as (me && r == rr) the compiler built the
