@@ -267,7 +267,7 @@ void* cg_engine_stream(cg_engine* engine);
  *   "max_waves", "wave_stride"  rate sampling only: run at most max_waves filter waves, every
  *                      wave_stride-th one; the result is then PARTIAL (stats.waves_run < waves_total)
  *   "fut_block"        1 (default) output-rank granularity of K4's future-service bound (exact counts)
- *   "lane_check"       32 (default) request-steps between K4's prune checks (8, 16, 32 or 64)
+ *   "lane_check"       32 (default) request-steps between K4's prune checks (32 or 64)
  *   "seeds"            1 (default) homogeneous plans of the heavy rows simulated first; 0 off
  *   "fut_bound", "item_plans", "k1_form", "overflow_capacity", "tie_capacity", "ub_oracle",
  *   "quality_block" (diagnostic)

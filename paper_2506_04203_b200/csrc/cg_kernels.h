@@ -139,6 +139,14 @@ constexpr unsigned long long kItemPlanMask = (1ull << kItemPlanBits) - 1ull;
 //            sojourn (k_plan_filter's header comment), already with its
 //            1e-12 margins: sojourns below it never reach the p95.
 constexpr int kRecMaxParts = 13;
+// request-steps per k_lane trip (prune checks every SimArgs::lane_check + 1
+// trips).  One trip per 32-step check interval: the per-trip bookkeeping
+// (claim/finish votes, the bound broadcast, check set-up) is paid once per
+// check (C3 K4: 4-step trips 265 ms, 8: 250, 16: 242, 32: 238)
+#ifndef CG_UNROLL
+#define CG_UNROLL 32
+#endif
+constexpr int kLaneUnroll = CG_UNROLL;
 struct ItemRec {
     unsigned long long item;   // (row << 44) | plan index
     unsigned long long w[3];

@@ -192,7 +192,7 @@ struct cg_engine {
     int fut_bound = 1;  // future-service bound in K4 (option fut_bound)
     int fut_block = 1;  // output-rank block of the future bound (option fut_block; 1 = exact counts)
     int fut_arrival_shift = 5;  // log2 arrival block of the future bound (option fut_arrival: 1, 2, 4, ..., 32)
-    int lane_check = 32;  // k_lane request-steps between prune checks (option lane_check: 8, 16, 32, 64)
+    int lane_check = 32;  // k_lane request-steps between prune checks (option lane_check: 32, 64)
     int pilot = 1;      // pilot plans per (row, budget) cell before the lists (option pilot: 1 auto, 2 on, 0 off)
     int seeds = 1;      // homogeneous seed plans of the heavy rows first (option seeds)
     long long pilot_min_plans = 0;  // rows with fewer plans get no pilot (option pilot_min_plans)
@@ -485,7 +485,7 @@ void evaluate_rows(SweepCtx& x, const std::vector<RowDesc>& rows, const std::vec
     base.sld = sld;
     base.counters = ctrs;
     base.ring_cap = ring_cap;
-    base.lane_check = (unsigned)(E.lane_check / 4 - 1);  // k_lane runs 4 request-steps per trip
+    base.lane_check = (unsigned)std::max(0, E.lane_check / kLaneUnroll - 1);  // k_lane runs kLaneUnroll request-steps per trip
 
     // Runs one packed work list through the class kernel; ring overflows are
     // appended to the class's overflow region.
@@ -2016,7 +2016,7 @@ cg_status cg_engine_set_option(cg_engine* e, const char* key, int64_t value) {
             e->fut_arrival_shift = sh;
         }
         else if (k == "lane_check") {
-            if (value != 8 && value != 16 && value != 32 && value != 64) fail(CG_ERR_INVALID_INPUT, "lane_check must be 8, 16, 32 or 64");
+            if (value != 32 && value != 64) fail(CG_ERR_INVALID_INPUT, "lane_check must be 32 or 64");
             e->lane_check = (int)value;
         }
         else if (k == "pilot") e->pilot = (int)std::min<int64_t>(2, std::max<int64_t>(0, value));

@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     using TR = LaneTraits<W, R>;
     constexpr int G = TR::G;
     constexpr int CAP = TR::CAP;
-    constexpr int UNROLL = 4;
+    constexpr int UNROLL = kLaneUnroll;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
