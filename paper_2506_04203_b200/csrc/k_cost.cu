@@ -34,6 +34,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "cg_cuda.h"
 #include "cg_internal.h"
@@ -151,8 +152,6 @@ struct GroupShared {
     int used;   // GPUs of the current count vector
     int dp;
     int status;
-    int has_item;
-    int dp_enum;  // replicas of the current count vector
     int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
     int qi;       // future-bound blocks of the plan (SimArgs::qtab)
     unsigned char pshape[kGsParts], pcount[kGsParts];
@@ -817,7 +816,7 @@ struct LaneTraits {
     // R = 16 / 32 (one lane holds a whole dp <= 32 plan): 4 slots, deeper
     // queues overflow to the DEEP re-run; 2-warp blocks pack shared memory
     static constexpr int CAP = R <= 4 ? 32 : (R <= 8 ? (W == 1 ? 8 : 16) : 4);
-    static constexpr int WPB = R >= 16 ? 2 : 4;  // warps per block
+    static constexpr int WPB = R >= 32 ? 1 : (R >= 16 ? 2 : 4);  // warps per block (R = 32: five 1-warp blocks per SM)
     // SA (R = 32): replica finish times in shared memory -- the idle mask is a
     // fully unrolled scan of loads and compares, the winner's update one store
     // (in registers it is a compare and two selects per replica per step) --
@@ -826,12 +825,17 @@ struct LaneTraits {
     static constexpr bool SA = W == 1 && R >= 32;
     // AS: replica finish times in shared memory (SA, and R >= CG_AS_MIN)
     static constexpr bool AS = W == 1 && R >= CG_AS_MIN;
-    static constexpr int PD = SA ? kGsParts : R;  // prefill/decode slots per lane
+    static constexpr int PD = SA ? kRecMaxParts : R;  // prefill/decode slots per lane (SA: per part)
     static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
     // prefill, decode, head-job finish, previous-job finish (per replica slot)
     static constexpr size_t pd_bytes = (size_t)(2 * PD + (AS ? 3 : 2) * R) * 32 * sizeof(double);
-    static constexpr size_t ht_bytes = (size_t)R * 32 * sizeof(unsigned);  // ring head | tail << 16
+    // ring head | tail << HS, both mod HM + 1: one byte per replica when the
+    // ring holds <= 4 jobs (lengths up to CAP + 1 < 16 stay distinguishable)
+    using HT = typename std::conditional<CAP <= 4, unsigned char, unsigned>::type;
+    static constexpr unsigned HS = CAP <= 4 ? 4u : 16u;
+    static constexpr unsigned HM = CAP <= 4 ? 0xfu : 0xffffu;
+    static constexpr size_t ht_bytes = (size_t)R * 32 * sizeof(HT);
     static constexpr size_t hist_bytes = 256 * sizeof(unsigned);
     static constexpr size_t bytes_per_warp = ring_bytes + pd_bytes + ht_bytes + hist_bytes + G * sizeof(GroupShared);
     static_assert(hist_bytes >= (size_t)G * kMaxShapes, "count-vector scratch in the histogram area");
@@ -1026,7 +1030,9 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
     // select per replica per step).
     double* prev_s = nd_s + R * 32;
     double* avail_s = prev_s + R * 32;  // SA: finish of each replica's last job
-    unsigned* ht_s = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes);
+    using HT = typename TR::HT;
+    constexpr unsigned HS = TR::HS, HM = TR::HM;
+    HT* ht_s = reinterpret_cast<HT*>(wbase + TR::ring_bytes + TR::pd_bytes);
     unsigned* hist = reinterpret_cast<unsigned*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes);
     GroupShared* gsa = reinterpret_cast<GroupShared*>(wbase + TR::ring_bytes + TR::pd_bytes + TR::ht_bytes +
                                                       TR::hist_bytes);
@@ -1188,7 +1194,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
             K4P_MARK(1);
             if (need) {
                 status = gs.status;
-                if (SA && status == ST_RUN && gs.nparts == 0) {
+                if (SA && status == ST_RUN && (gs.nparts == 0 || gs.nparts > TR::PD)) {
                     // more parts than the per-part tables hold: the DEEP re-run takes it
                     const unsigned long long idx = atomicAdd(a.ovf_count, 1ull);
                     if (idx < a.ovf_cap) a.ovf[idx] = ((unsigned long long)gs.row << kItemPlanBits) | gs.plan;
@@ -1370,7 +1376,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                             if (lz) {
                                 nd_s[r * 32 + lane] = av_get(r);
                                 const unsigned hr = ht_s[r * 32 + lane];
-                                ht_s[r * 32 + lane] = (hr & 0xffff0000u) | (hr >> 16);
+                                ht_s[r * 32 + lane] = (HT)((hr & (HM << HS)) | ((hr >> HS) & HM));
                             }
                         }
                         lazy = 0;
@@ -1384,8 +1390,8 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                         for (int r = 0; r < R; ++r) {
                             if (!((dep >> r) & 1u)) continue;
                             const unsigned hr = ht_s[r * 32 + lane];
-                            const unsigned h = hr & 0xffffu;
-                            const unsigned tl = hr >> 16;
+                            const unsigned h = hr & HM;
+                            const unsigned tl = (hr >> HS) & HM;
                             const bool more = h != tl;  // the head waiting job enters service
                             double oh = 0.0;
                             if (HO) oh = ho[r];
@@ -1395,8 +1401,8 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                             const double nx = __dadd_rn(__dadd_rn(ndr, pre_s[pr]), __dmul_rn(oh, dec_s[pr]));
                             const double nn = more ? nx : INF;
                             nd_s[r * 32 + lane] = nn;
-                            const unsigned h1 = (h + 1u) & 0xffffu;
-                            if (more) ht_s[r * 32 + lane] = (hr & 0xffff0000u) | h1;
+                            const unsigned h1 = (h + 1u) & HM;
+                            if (more) ht_s[r * 32 + lane] = (HT)((hr & (HM << HS)) | h1);
                             if (HO && more && h1 != tl) ho[r] = Orow[ring[(r * CAP + (int)(h1 & (CAP - 1))) * 32 + lane]];
                             dep = (nn <= t) ? dep : (dep & ~(1u << r));
                         }
@@ -1407,7 +1413,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     for (int r = 0; r < R; ++r) {
                         const int j = gl * R + r;
                         const unsigned hr = ht_s[r * 32 + lane];
-                        const unsigned c = (((hr >> 16) - hr) & 0xffffu) + (nd_s[r * 32 + lane] < INF ? 1u : 0u);
+                        const unsigned c = (((hr >> HS) - hr) & HM) + (nd_s[r * 32 + lane] < INF ? 1u : 0u);
                         kk[r] = (j < dp) ? ((c << 9) | (unsigned)j) : 0xffffffffu;
                     }
 #pragma unroll
@@ -1455,21 +1461,21 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                 // job in service (finishing at start) and this one waiting --
                 // the ring restarts empty.  Otherwise the job joins the queue.
                 if (me && one) {
-                    H = (H & 0xffff0000u) | (H >> 16);
+                    H = (H & (HM << HS)) | ((H >> HS) & HM);
                     nd_s[rr * 32 + lane] = start;
                     lazy &= ~(1u << rr);
                 }
                 const bool push = me && !idle;
-                const bool first = push && ((H >> 16) == (H & 0xffffu));  // the ring was empty
-                if (push) ring[(rr * CAP + (int)((H >> 16) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
-                H += push ? (1u << 16) : 0u;
-                ovf |= push && ((((H >> 16) - H) & 0xffffu) > (unsigned)CAP);
+                const bool first = push && (((H >> HS) & HM) == (H & HM));  // the ring was empty
+                if (push) ring[(rr * CAP + (int)((H >> HS) & (CAP - 1))) * 32 + lane] = (unsigned short)k;
+                H += push ? (1u << HS) : 0u;
+                ovf |= push && ((((H >> HS) - H) & HM) > (unsigned)CAP);
                 lazy |= (me && idle) ? (1u << rr) : 0u;
                 // prev = start: the old finish when busy; when idle any value
                 // <= t (every later test is prev <= t' with t' >= t)
                 if (me) {
                     prev_s[rr * 32 + lane] = start;
-                    ht_s[rr * 32 + lane] = H;
+                    ht_s[rr * 32 + lane] = (HT)H;
                 }
                 if constexpr (AS) {
                     if (me) avail_s[rr * 32 + lane] = fin;
