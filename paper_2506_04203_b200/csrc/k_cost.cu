@@ -816,7 +816,9 @@ struct LaneTraits {
     // R = 16 / 32 (one lane holds a whole dp <= 32 plan): 4 slots, deeper
     // queues overflow to the DEEP re-run; 2-warp blocks pack shared memory
     static constexpr int CAP = R <= 4 ? 32 : (R <= 8 ? (W == 1 ? 8 : 16) : 4);
-    static constexpr int WPB = R >= 32 ? 1 : (R >= 16 ? 2 : 4);  // warps per block (R = 32: five 1-warp blocks per SM)
+    // warps per block: R = 32 five 1-warp blocks per SM, R = 16 four 2-warp blocks (1-warp blocks when its
+    // finish times are in shared memory, CG_AS_MIN = 16)
+    static constexpr int WPB = R >= 32 ? 1 : (R >= 16 ? (W == 1 && R >= CG_AS_MIN ? 1 : 2) : 4);
     // SA (R = 32): replica finish times in shared memory -- the idle mask is a
     // fully unrolled scan of loads and compares, the winner's update one store
     // (in registers it is a compare and two selects per replica per step) --
