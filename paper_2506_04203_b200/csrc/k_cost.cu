@@ -142,24 +142,26 @@ enum : int { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2, ST_FINISH = 3 };
 #ifndef CG_AS_MIN
 #define CG_AS_MIN 32
 #endif
-constexpr int kGsParts = 16;  // parts held in GroupShared (>= kRecMaxParts)
+constexpr int kGsParts = kRecMaxParts;  // parts held in GroupShared (more: counts[] stay authoritative)
 
 struct GroupShared {
     unsigned long long plan;  // current plan index
     unsigned long long hi;    // k_lane: the pre-claimed next record's item (cp.async target)
     double lbk;   // the plan's service bound: sojourns below it never reach the p95
     int row;
-    int used;   // GPUs of the current count vector
-    int dp;
-    int status;
-    int nparts;   // > 0: the plan's (shape, count) parts below, in shape order
-    int qi;       // future-bound blocks of the plan (SimArgs::qtab)
+    int used;                // GPUs of the current count vector
+    unsigned short dp;       // replicas (<= 255)
+    unsigned short qi;       // future-bound blocks of the plan (SimArgs::qtab, a u16 count)
+    unsigned char nparts;    // > 0: the plan's (shape, count) parts below, in shape order
+    unsigned char status;
+    unsigned ps;             // k_lane: bit j set when replica j starts a part (parts listed)
     unsigned char pshape[kGsParts], pcount[kGsParts];
     union {
         unsigned char counts[kMaxShapes];  // k_sim: count vector of the current plan
         unsigned long long pfw[4];         // k_lane: the next record's parts words and service bound
     };
 };
+static_assert(sizeof(GroupShared) == 104, "GroupShared layout (k_lane shared-memory budget)");
 
 // ItemRec part stream (cg_kernels.h): header (np, used) then 13-bit parts.
 __device__ __forceinline__ void encode_rec(ItemRec& r, const unsigned char* c, int S, int used) {
@@ -865,6 +867,7 @@ __device__ bool lane_take_r(const SimArgs& a, GroupShared& gs, unsigned char* co
         // the part offsets are constants) and issue the live bound and every
         // part's bound-snapshot entry at once -- independent loads, one latency
         unsigned shp[kRecMaxParts];
+        unsigned ps = 0u;  // part starts, from the counts in registers
 #pragma unroll
         for (int q = 0; q < kRecMaxParts; ++q) {
             shp[q] = 0u;
@@ -873,9 +876,11 @@ __device__ bool lane_take_r(const SimArgs& a, GroupShared& gs, unsigned char* co
                 shp[q] = v & 31u;
                 gs.pshape[q] = (unsigned char)(v & 31u);
                 gs.pcount[q] = (unsigned char)(v >> 5);
+                if (dp < 32) ps |= 1u << dp;
                 dp += (int)(v >> 5);
             }
         }
+        gs.ps = ps;
         used = (int)((w0 >> 4) & 511ull);
         const long long cell = (long long)row * (a.N + 1) + used;
         const double U = a.prune ? __longlong_as_double((long long)*(volatile unsigned long long*)&a.ub[cell])
@@ -901,11 +906,13 @@ __device__ bool lane_take_r(const SimArgs& a, GroupShared& gs, unsigned char* co
         gs.lbk = lb;
         return true;
     }
+    unsigned ps = 0u;
     if (np > 0) {
         for (int q = 0; q < np; ++q) {
             const unsigned v = rec_part(w0, w1, w2, q);
             gs.pshape[q] = (unsigned char)(v & 31u);
             gs.pcount[q] = (unsigned char)(v >> 5);
+            if (dp < 32) ps |= 1u << dp;
             dp += (int)(v >> 5);
         }
         used = (int)((w0 >> 4) & 511ull);
@@ -918,11 +925,13 @@ __device__ bool lane_take_r(const SimArgs& a, GroupShared& gs, unsigned char* co
                 gs.pshape[np] = (unsigned char)s;
                 gs.pcount[np] = (unsigned char)c;
             }
+            if (dp < 32) ps |= 1u << dp;
             ++np;
             dp += c;
         }
         if (np > kGsParts) np = 0;  // counts[] stay authoritative
     }
+    gs.ps = ps;
     if (a.check_stable) {  // seeds are not pre-filtered (costmodel.cpp:366-376)
         double capacity = 0.0;
         for (int q = 0, s = 0; np > 0 ? q < np : s < sp.S; np > 0 ? ++q : ++s) {
@@ -1228,13 +1237,7 @@ __global__ void __launch_bounds__(LaneTraits<W, R>::WPB * 32, LaneTraits<W, R>::
                     const int np = gs.nparts;
                     unsigned ps = 0u;  // bit j: replica j starts a part
                     if (np > 0) {
-                        int c0 = 0;
-#pragma unroll
-                        for (int qq = 0; qq < kGsParts; ++qq)
-                            if (qq < np) {
-                                if (c0 < 32) ps |= 1u << c0;
-                                c0 += gs.pcount[qq];
-                            }
+                        ps = gs.ps;  // the claim built it from the counts in registers
                         if (SA) {
 #pragma unroll
                             for (int qq = 0; qq < kGsParts; ++qq)
