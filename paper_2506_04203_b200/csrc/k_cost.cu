@@ -142,7 +142,7 @@ enum : int { ST_NEED = 0, ST_RUN = 1, ST_DONE = 2, ST_FINISH = 3 };
 #ifndef CG_AS_MIN
 #define CG_AS_MIN 32
 #endif
-constexpr int kGsParts = kRecMaxParts;  // parts held in GroupShared (more: counts[] stay authoritative)
+constexpr int kGsParts = 16;  // parts held in GroupShared (>= kRecMaxParts; more: counts[] stay authoritative)
 
 struct GroupShared {
     unsigned long long plan;  // current plan index
@@ -161,7 +161,7 @@ struct GroupShared {
         unsigned long long pfw[4];         // k_lane: the next record's parts words and service bound
     };
 };
-static_assert(sizeof(GroupShared) == 104, "GroupShared layout (k_lane shared-memory budget)");
+static_assert(sizeof(GroupShared) == 112, "GroupShared layout (k_lane shared-memory budget)");
 
 // ItemRec part stream (cg_kernels.h): header (np, used) then 13-bit parts.
 __device__ __forceinline__ void encode_rec(ItemRec& r, const unsigned char* c, int S, int used) {
@@ -829,7 +829,10 @@ struct LaneTraits {
     static constexpr bool SA = W == 1 && R >= 32;
     // AS: replica finish times in shared memory (SA, and R >= CG_AS_MIN)
     static constexpr bool AS = W == 1 && R >= CG_AS_MIN;
-    static constexpr int PD = SA ? kRecMaxParts : R;  // prefill/decode slots per lane (SA: per part)
+    // prefill/decode slots per lane (SA: per part, up to 16 parts -- plans of up to 16 parts run here; with
+    // 13 slots the dp 17-32 kernel fits five blocks per SM, but 14-16-part plans then all go to the DEEP
+    // re-run and exhaust its list on wide shape sets such as C5's)
+    static constexpr int PD = SA ? kGsParts : R;
     static constexpr int MIN_BLOCKS = 1;
     static constexpr size_t ring_bytes = (size_t)R * CAP * 32 * sizeof(unsigned short);
     // prefill, decode, head-job finish, previous-job finish (per replica slot)
